@@ -1,0 +1,246 @@
+/* gsg.h -- C ABI of libgsg.so: the B200 (sm_100a) hot path of graph-sampling GCN training.
+ *
+ * The operation (arXiv 2010.03166, "Accurate, Efficient and Scalable Training of Graph
+ * Neural Networks"; PAPER.md line numbers as P:n):
+ *   per sampled subgraph G_s (Alg. 1 lines 3-6) build the normalized adjacency
+ *   Â_s (Eq. 5) and its transpose (Alg. 4); then per GCN layer l
+ *     forward  (Eq. 5):           P = Â X ;  H = ReLU(P W)
+ *     backward (Eq. 13 at P:704):  dZ = dH ⊙ 1[H > 0] ;  dW = Pᵀ dZ ;
+ *                                         dX = Âᵀ (dZ Wᵀ)
+ *   plus the classifier head (Eqs. 2-4; backward Eqs. 9-11) and the
+ *   data-parallel mean of dW over independent subgraphs.
+ *
+ * Conventions (all entry points):
+ *   - Return value: GSG_OK (0) or a negative GSG_E* code; a human-readable message for the
+ *     calling thread is available from gsg_last_error() until its next failing call.
+ *   - Argument errors (shapes, strides, alignment, NULL pointers) are reported
+ *     synchronously and nothing is launched. Kernels are stream-ordered on the context's
+ *     stream; asynchronous CUDA faults surface from the next call or from gsg_ctx_sync().
+ *   - Dense matrices are row-major. `ld*` is the row stride in ELEMENTS, ld >= columns, and
+ *     ld * sizeof(elem) must be a multiple of 16 bytes (TMA); base pointers 16-byte aligned.
+ *     Columns [f, round_up(f, 4)) of an fp32 output row may be overwritten (float4 stores);
+ *     columns beyond that are never touched.
+ *   - Pointers named d_* / matrices passed to layer calls are DEVICE pointers owned by the
+ *     caller. Pointers named h_* are host pointers (pinned memory enables async copies).
+ *   - The library owns every subgraph array and the per-context workspace (split-K partials,
+ *     T = dZ Wᵀ scratch, bf16 weight copies). Host inputs are copied, never retained.
+ *   - Threading: one context per host thread/stream. Distinct subgraphs may be used
+ *     concurrently from distinct contexts on the same device.
+ *   - No CPU fallback exists: every compute step runs in this library's sm_100a kernels.
+ */
+#ifndef GSG_H_
+#define GSG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define GSG_API __attribute__((visibility("default")))
+#else
+#define GSG_API
+#endif
+
+/* ---- status codes -------------------------------------------------------------------- */
+enum {
+  GSG_OK = 0,
+  GSG_EINVAL = -1,         /* bad shape / stride / alignment / pointer / enum value        */
+  GSG_EGRAPH = -2,         /* CSR invariant violated (see gsg_subgraph_upload)             */
+  GSG_ENOMEM = -3,         /* device allocation failed                                     */
+  GSG_ECUDA = -4,          /* CUDA runtime/driver error (message has the CUDA string)      */
+  GSG_ENCCL = -5,          /* NCCL error or NCCL library not loadable                      */
+  GSG_EUNSUPPORTED = -6    /* device is not sm_100, or a size exceeds a 32-bit index       */
+};
+
+/* ---- normalization modes (gsg_subgraph_normalize) ------------------------------------ */
+enum {
+  GSG_NORM_ROW_SELF = 0,   /* Â = D~^-1 (A + I), D~ = D + I, subgraph-local degrees: the
+                              BASELINE configs (SURVEY reading R1/R2); rows sum to 1       */
+  GSG_NORM_SYM_SELF = 1,   /* Â = (I+D)^-1/2 (I+A) (I+D)^-1/2, Eq. 5               */
+  GSG_NORM_ROW = 2,        /* Ã = D^-1 A, GraphSAGE Eq. 1; isolated rows are zero  */
+  GSG_NORM_VALUES = 3      /* Â_ij = the uploaded edge values, no self loop (weighted /
+                              GraphSAINT-normalized adjacency)                  */
+};
+
+/* ---- GEMM precision ------------------------------------------------------------------ */
+enum {
+  GSG_PREC_TF32 = 0,       /* fp32 operands read as TF32 by tcgen05 (kind::tf32), fp32 acc */
+  GSG_PREC_BF16 = 1        /* bf16 operand copies (kind::f16), fp32 accumulate             */
+};
+
+/* ---- flags --------------------------------------------------------------------------- */
+enum {
+  GSG_NO_RELU = 1,         /* forward: H = P W (no ReLU)                                   */
+  GSG_DH_PREMASKED = 2,    /* backward: dH already equals dZ = dH ⊙ 1[H>0] (fused upstream) */
+  GSG_ACCUM_DW = 4         /* backward: dW += Pᵀ dZ instead of dW = Pᵀ dZ                  */
+};
+
+/* ---- GEMM epilogues (gsg_gemm) ------------------------------------------------------- */
+enum {
+  GSG_EPI_NONE = 0,        /* C = op(A) op(B)                                              */
+  GSG_EPI_RELU = 1,        /* C = max(op(A) op(B), 0)               (forward a3)           */
+  GSG_EPI_MASK = 2         /* C = (op(A) op(B)) ⊙ 1[aux > 0]         (ReLU' gate, a4)       */
+};
+
+/* ---- head kinds ---------------------------------------------------------------------- */
+enum { GSG_HEAD_SOFTMAX = 0, GSG_HEAD_SIGMOID = 1 };
+
+typedef struct gsg_ctx* gsg_ctx_t;
+typedef struct gsg_subgraph* gsg_subgraph_t;
+
+/* ==== context ========================================================================== */
+/* Create a context on CUDA device `device`, issuing work on `cuda_stream` (a cudaStream_t,
+ * not owned; NULL = the legacy default stream, which also orders against torch's default
+ * stream). Fails with
+ * GSG_EUNSUPPORTED if the device is not compute capability 10.0 (sm_100a kernels only). */
+GSG_API int gsg_ctx_create(int device, void* cuda_stream, gsg_ctx_t* out);
+GSG_API int gsg_ctx_destroy(gsg_ctx_t ctx);
+/* Re-target subsequent launches to another stream (e.g. torch's current stream). */
+GSG_API int gsg_ctx_set_stream(gsg_ctx_t ctx, void* cuda_stream);
+GSG_API void* gsg_ctx_stream(gsg_ctx_t ctx);
+/* Block until the context's stream drains; returns GSG_ECUDA for any pending fault. */
+GSG_API int gsg_ctx_sync(gsg_ctx_t ctx);
+/* Number of kernels this context has launched so far (evidence counter for benches). */
+GSG_API int64_t gsg_ctx_launch_count(gsg_ctx_t ctx);
+/* Thread-local message of the last failing call on this thread ("" if none). */
+GSG_API const char* gsg_last_error(void);
+
+/* ==== subgraph =================================================== */
+/* Copy an induced subgraph G_s (Alg. 2 line 9) to the device.
+ *   n            number of subgraph nodes |V_s| (0 <= n < 2^31)
+ *   nnz          number of stored directed entries of A_s (no self loops)
+ *   h_indptr     host int64[n+1], h_indptr[0] = 0, non-decreasing, h_indptr[n] = nnz
+ *   h_indices    host int32[nnz]; row i = h_indices[h_indptr[i] .. h_indptr[i+1])
+ *   h_values     host float[nnz] edge weights, or NULL for a binary adjacency (required by
+ *                GSG_NORM_VALUES, ignored by the degree-based modes)
+ *   validate     1 = check on the host before copying, rejecting with GSG_EGRAPH (first
+ *                offending entry in the message): an index out of [0, n); a row that is not
+ *                strictly ascending (Alg. 4's precondition; this also rejects
+ *                duplicates); a self loop (normalization adds it); an asymmetric
+ *                structure (the undirected assumption of P:737-743).
+ * The structure must satisfy those invariants even when validate = 0 (undefined results
+ * otherwise). nnz + n must be < 2^31. On success *out owns device copies. */
+GSG_API int gsg_subgraph_upload(gsg_ctx_t ctx, int32_t n, int64_t nnz, const int64_t* h_indptr,
+                                const int32_t* h_indices, const float* h_values, int validate,
+                                gsg_subgraph_t* out);
+/* Same, from DEVICE arrays already resident in HBM (stream-ordered device-to-device copy;
+ * no validation). Used when a pool of subgraphs lives on the GPU (Alg. 7 pool). */
+GSG_API int gsg_subgraph_upload_device(gsg_ctx_t ctx, int32_t n, int64_t nnz,
+                                       const int64_t* d_indptr, const int32_t* d_indices,
+                                       const float* d_values, gsg_subgraph_t* out);
+/* Build Â on the device (stream-ordered, no host synchronization):
+ *   - insert the self loop of each row at its sorted position (*_SELF modes),
+ *   - values per `norm_mode` (GSG_NORM_*), computed in fp64 and rounded to fp32,
+ *   - the transposed values valT on the same (symmetric) structure: valT at slot (u, v)
+ *     equals val at slot (v, u) -- a device gather form of Alg. 4 that yields
+ *     exactly Alg. 4's DataTrans (a permutation of val),
+ *   - degree bins (rows ordered by degree, heavy rows split across warps in the SpMMs).
+ * May be called again with another mode. */
+GSG_API int gsg_subgraph_normalize(gsg_ctx_t ctx, gsg_subgraph_t sg, int norm_mode);
+/* Sizes of the normalized subgraph. Synchronizes the stream (reads device counters). */
+GSG_API int gsg_subgraph_info(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t* n, int64_t* nnz_hat,
+                              int32_t* max_deg_hat, int32_t* n_heavy);
+/* Copy Â back to the host (tests): h_indptr int64[n+1], h_idx int32[nnz_hat],
+ * h_val / h_valT float[nnz_hat]; any pointer may be NULL. Synchronizes. */
+GSG_API int gsg_subgraph_download(gsg_ctx_t ctx, gsg_subgraph_t sg, int64_t* h_indptr,
+                                  int32_t* h_idx, float* h_val, float* h_valT);
+GSG_API int gsg_subgraph_free(gsg_subgraph_t sg);
+
+/* ==== sparse aggregation (rows a2 / a7) ================================================ */
+/* Y = Â X (transpose = 0, P = Â X of Eq. 5 / Alg. 6) or Y = Âᵀ X (transpose = 1,
+ * the backward dX = Âᵀ T of P:719, read from valT). fp32 in, fp32 accumulate, fp32 out.
+ *   f            feature width (columns) of X and Y, 1 <= f
+ *   d_X, ldx     n x f input (ldx % 4 == 0)
+ *   d_Y, ldy     n x f output (ldy % 4 == 0), must not alias d_X
+ *   d_Ylp, ldylp optional bf16 copy of Y (NULL = none; ldylp % 8 == 0)
+ *   d_mask, ldm  optional ReLU' gate: Y ⊙ 1[mask > 0] (NULL = none) -- used to emit the
+ *                next layer's dZ directly from the transposed aggregation
+ * Each output row is summed in a fixed order (bitwise reproducible run to run). */
+GSG_API int gsg_spmm(gsg_ctx_t ctx, gsg_subgraph_t sg, int transpose, int32_t f,
+                     const float* d_X, int64_t ldx, float* d_Y, int64_t ldy,
+                     void* d_Ylp, int64_t ldylp, const float* d_mask, int64_t ldm);
+
+/* ==== dense contraction on tcgen05 tensor cores (rows a3 / a5 / a6) ==================== */
+/* C[M x N] = epi( op(A) op(B) ), fp32 accumulate in TMEM.
+ *   op(A): transA = 0 -> A stored M x K row-major (lda >= K); transA = 1 -> A stored K x M
+ *          (lda >= M), i.e. op(A) = Aᵀ. Same for B: transB = 0 -> K x N (ldb >= N);
+ *          transB = 1 -> stored N x K (ldb >= K).
+ *   precision    GSG_PREC_TF32: A, B are float*; GSG_PREC_BF16: A, B are bf16 (uint16) *
+ *   d_C, ldc     fp32 output; d_Clp, ldclp optional bf16 copy (NULL = none)
+ *   epilogue     GSG_EPI_*; d_aux/ldaux is the M x N gate for GSG_EPI_MASK
+ *   split_k      0 = automatic; >= 1 forces the number of K splits (deterministic fixed-order
+ *                reduction through the context workspace)
+ *   accumulate   1 = C += result (before the epilogue is NOT supported with RELU/MASK)
+ * K = 0 writes epi(0). */
+GSG_API int gsg_gemm(gsg_ctx_t ctx, int32_t M, int32_t N, int32_t K,
+                     const void* d_A, int64_t lda, int transA,
+                     const void* d_B, int64_t ldb, int transB,
+                     float* d_C, int64_t ldc, void* d_Clp, int64_t ldclp,
+                     int precision, int epilogue, const float* d_aux, int64_t ldaux,
+                     int split_k, int accumulate);
+
+/* fp32 -> bf16 copy of a rows x cols matrix (round-to-nearest-even). */
+GSG_API int gsg_to_bf16(gsg_ctx_t ctx, int32_t rows, int32_t cols, const float* d_src,
+                        int64_t lds, void* d_dst, int64_t ldd);
+
+/* ==== GCN layer (Eq. 5 forward, P:719 backward) ======================================== */
+/* Forward: P = Â X (kept for backward), H = ReLU(P W) (GSG_NO_RELU: H = P W).
+ *   X (n x f_in, ldx), W (f_in x f_out row-major, ldw), P (n x f_in, ldp), H (n x f_out, ldh)
+ *   precision = GSG_PREC_BF16 additionally needs P_lp (bf16 n x f_in, ldplp) which the
+ *   aggregation writes for the GEMM; H_lp (bf16 n x f_out) is optional.
+ * Chain order (ÂX)W is fixed (SURVEY §8(a) notes; §7.1 P:923-934 order choice is NEXT). */
+GSG_API int gsg_layer_forward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, int32_t f_out,
+                              const float* d_X, int64_t ldx, const float* d_W, int64_t ldw,
+                              float* d_P, int64_t ldp, void* d_Plp, int64_t ldplp,
+                              float* d_H, int64_t ldh, void* d_Hlp, int64_t ldhlp,
+                              int precision, int flags);
+/* Backward of one layer given the forward's P and H:
+ *   dZ = dH ⊙ 1[H > 0] (skipped with GSG_DH_PREMASKED: dH is dZ),
+ *   dW = Pᵀ dZ          (f_in x f_out; GSG_ACCUM_DW adds into dW),
+ *   dX = Âᵀ (dZ Wᵀ)     (n x f_in; d_dX = NULL skips it, e.g. for layer 1),
+ *        ⊙ 1[H_below > 0] when d_Hbelow != NULL, i.e. dX is then the layer below's dZ.
+ * BF16: d_Plp (bf16 P) is required; d_dHlp (bf16 copy of the premasked dH) is optional;
+ * d_dXlp (bf16 copy of dX) is optional. T = dZ Wᵀ and masked-dZ live in the workspace. */
+GSG_API int gsg_layer_backward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, int32_t f_out,
+                               const float* d_P, int64_t ldp, const void* d_Plp, int64_t ldplp,
+                               const float* d_H, int64_t ldh,
+                               const float* d_dH, int64_t lddh, const void* d_dHlp, int64_t lddhlp,
+                               const float* d_W, int64_t ldw,
+                               float* d_dW, int64_t lddw,
+                               float* d_dX, int64_t lddx, void* d_dXlp, int64_t lddxlp,
+                               const float* d_Hbelow, int64_t ldhb,
+                               int precision, int flags);
+
+/* ==== classifier head + CE loss (SUPPORT row a8) ======================================= */
+/* S = H_L W_mlp ; S+ = ReLU(S) ; Y = softmax_rows(S+) (GSG_HEAD_SOFTMAX, labels int32[n]
+ * class ids) or sigmoid(S+) (GSG_HEAD_SIGMOID, labels uint8[n x C] indicators, ld C);
+ * loss = mean CE over the n rows (readings R7/R8);
+ * dS = (Y - Ybar)/n ⊙ 1[S > 0] ; dW_mlp = H_Lᵀ dS ; dH_L = (dS W_mlpᵀ) ⊙ 1[H_L > 0]
+ * (the returned dH_L is the top GCN layer's dZ, i.e. already premasked).
+ *   d_S, d_dS    n x C fp32 scratch/outputs (ld lds); d_loss: one device float.
+ *   d_dHlp       optional bf16 copy of dH_L (for BF16 layer backward). */
+GSG_API int gsg_head(gsg_ctx_t ctx, int32_t n, int32_t f, int32_t C, int kind,
+                     const float* d_HL, int64_t ldh, const float* d_Wmlp, int64_t ldw,
+                     const void* d_labels, float* d_S, float* d_dS, int64_t lds,
+                     float* d_dWmlp, int64_t lddw, float* d_dHL, int64_t lddh,
+                     void* d_dHlp, int64_t lddhlp, float* d_loss, int precision);
+
+/* ==== data parallelism (row a9) ======================================================== */
+/* NCCL plumbing (libnccl.so.2 is resolved at run time; the process's already-loaded copy,
+ * e.g. torch's, is reused). The 128-byte unique id is produced on one rank and broadcast
+ * by the caller (torch.distributed). */
+GSG_API int gsg_nccl_unique_id(void* out_id128);
+GSG_API int gsg_nccl_comm_init(gsg_ctx_t ctx, int nranks, int rank, const void* id128,
+                               void** out_comm);
+GSG_API int gsg_nccl_comm_destroy(void* comm);
+/* Sum (average = 1: mean) of each buffer across the communicator's ranks, in place, on the
+ * context stream: bufs[i] (device fp32) has counts[i] elements. One grouped call. */
+GSG_API int gsg_allreduce_grads(gsg_ctx_t ctx, void* nccl_comm, float* const* bufs,
+                                const int64_t* counts, int nbufs, int average);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSG_H_ */

@@ -1,0 +1,493 @@
+// api.cu -- the C ABI of libgsg.so (include/gsg.h): argument checking, ownership, and the
+// composition of the hot-path kernels into the paper's per-layer calls.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdarg>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace gsg {
+
+static thread_local char g_err[2048] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(e == cudaErrorMemoryAllocation ? GSG_ENOMEM : GSG_ECUDA, "%s: %s (%s)", what, cudaGetErrorString(e),
+              cudaGetErrorName(e));
+}
+
+}  // namespace gsg
+
+using namespace gsg;
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int check_ctx(gsg_ctx_t c) { return c ? GSG_OK : fail(GSG_EINVAL, "NULL context"); }
+
+// ---- host-side CSR validation (gsg.h: gsg_subgraph_upload) ----
+int validate_csr(int32_t n, int64_t nnz, const int64_t* ip, const int32_t* ix) {
+  if (ip[0] != 0) return fail(GSG_EGRAPH, "indptr[0] = %lld, expected 0", (long long)ip[0]);
+  for (int32_t i = 0; i < n; i++)
+    if (ip[i + 1] < ip[i]) return fail(GSG_EGRAPH, "indptr decreases at row %d", i);
+  if (ip[n] != nnz) return fail(GSG_EGRAPH, "indptr[n] = %lld != nnz = %lld", (long long)ip[n], (long long)nnz);
+  for (int32_t i = 0; i < n; i++) {
+    for (int64_t k = ip[i]; k < ip[i + 1]; k++) {
+      const int32_t j = ix[k];
+      if (j < 0 || j >= n) return fail(GSG_EGRAPH, "edge (%d, %d): index out of range [0, %d)", i, j, n);
+      if (j == i) return fail(GSG_EGRAPH, "edge (%d, %d): self loop (normalization adds it)", i, j);
+      if (k > ip[i] && ix[k - 1] >= j)
+        return fail(GSG_EGRAPH, "edge (%d, %d): row %d not strictly ascending (previous %d)", i, j, i, ix[k - 1]);
+    }
+  }
+  for (int32_t i = 0; i < n; i++) {
+    for (int64_t k = ip[i]; k < ip[i + 1]; k++) {
+      const int32_t j = ix[k];
+      int64_t lo = ip[j], hi = ip[j + 1] - 1;
+      bool found = false;
+      while (lo <= hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (ix[mid] == i) { found = true; break; }
+        if (ix[mid] < i) lo = mid + 1; else hi = mid - 1;
+      }
+      if (!found) return fail(GSG_EGRAPH, "edge (%d, %d) has no reverse edge (%d, %d): not symmetric", i, j, j, i);
+    }
+  }
+  return GSG_OK;
+}
+
+int alloc_subgraph(gsg_ctx* ctx, int32_t n, int64_t nnz, bool has_values, gsg_subgraph** out) {
+  GSG_CHECK(n >= 0 && nnz >= 0, GSG_EINVAL, "negative n or nnz");
+  GSG_CHECK(nnz + (int64_t)n < (int64_t)INT32_MAX, GSG_EUNSUPPORTED, "nnz + n exceeds int32 indexing");
+  auto* sg = new gsg_subgraph;
+  sg->device = ctx->device;
+  sg->n = n;
+  sg->nnz = nnz;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](void** p, size_t b) { if (e == cudaSuccess) e = cudaMalloc(p, b > 0 ? b : 16); };
+  A((void**)&sg->indptr, sizeof(int64_t) * (n + 1));
+  A((void**)&sg->indices, sizeof(int32_t) * nnz);
+  if (has_values) A((void**)&sg->values, sizeof(float) * nnz);
+  A((void**)&sg->rowptr, sizeof(int32_t) * (n + 1));
+  A((void**)&sg->perm, sizeof(int32_t) * n);
+  A((void**)&sg->counters, sizeof(int32_t) * (3 * kBins + 8));
+  if (e != cudaSuccess) {
+    gsg_subgraph_free(sg);
+    return cuda_fail(e, "cudaMalloc(subgraph)");
+  }
+  *out = sg;
+  return GSG_OK;
+}
+
+// ---- NCCL (resolved at run time) ----
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+Nccl& nccl() {
+  static Nccl N;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      N.GetUniqueId = (decltype(N.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      N.CommInitRank = (decltype(N.CommInitRank))dlsym(h, "ncclCommInitRank");
+      N.CommDestroy = (decltype(N.CommDestroy))dlsym(h, "ncclCommDestroy");
+      N.AllReduce = (decltype(N.AllReduce))dlsym(h, "ncclAllReduce");
+      N.GroupStart = (decltype(N.GroupStart))dlsym(h, "ncclGroupStart");
+      N.GroupEnd = (decltype(N.GroupEnd))dlsym(h, "ncclGroupEnd");
+      N.GetErrorString = (decltype(N.GetErrorString))dlsym(h, "ncclGetErrorString");
+      N.ok = N.GetUniqueId && N.CommInitRank && N.CommDestroy && N.AllReduce && N.GroupStart && N.GroupEnd &&
+             N.GetErrorString;
+    }
+  }
+  return N;
+}
+
+int nccl_fail(ncclResult_t r, const char* what) {
+  return fail(GSG_ENCCL, "%s: %s", what, nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error");
+}
+
+int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+extern "C" {
+
+GSG_API const char* gsg_last_error(void) { return g_err; }
+
+GSG_API int gsg_ctx_create(int device, void* cuda_stream, gsg_ctx_t* out) {
+  GSG_CHECK(out, GSG_EINVAL, "out is NULL");
+  *out = nullptr;
+  int count = 0;
+  GSG_CUDA(cudaGetDeviceCount(&count));
+  GSG_CHECK(device >= 0 && device < count, GSG_EINVAL, "device %d out of range (%d devices)", device, count);
+  cudaDeviceProp prop;
+  GSG_CUDA(cudaGetDeviceProperties(&prop, device));
+  GSG_CHECK(prop.major == 10 && prop.minor == 0, GSG_EUNSUPPORTED,
+            "device %d is sm_%d%d; libgsg is built for sm_100a (B200) only", device, prop.major, prop.minor);
+  DeviceGuard dg(device);
+  auto* c = new gsg_ctx;
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  c->stream = static_cast<cudaStream_t>(cuda_stream);
+  *out = c;
+  return GSG_OK;
+}
+
+GSG_API int gsg_ctx_destroy(gsg_ctx_t c) {
+  if (!c) return GSG_OK;
+  DeviceGuard dg(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->ws_splitk.release(); c->ws_T.release(); c->ws_dZ.release();
+  c->ws_lp0.release(); c->ws_lp1.release(); c->ws_lp2.release(); c->ws_loss.release();
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return GSG_OK;
+}
+
+GSG_API int gsg_ctx_set_stream(gsg_ctx_t c, void* s) {
+  if (int rc = check_ctx(c)) return rc;
+  if (c->own_stream) { cudaStreamDestroy(c->stream); c->own_stream = false; }
+  c->stream = static_cast<cudaStream_t>(s);
+  return GSG_OK;
+}
+
+GSG_API void* gsg_ctx_stream(gsg_ctx_t c) { return c ? (void*)c->stream : nullptr; }
+
+GSG_API int gsg_ctx_sync(gsg_ctx_t c) {
+  if (int rc = check_ctx(c)) return rc;
+  DeviceGuard dg(c->device);
+  GSG_CUDA(cudaStreamSynchronize(c->stream));
+  GSG_CUDA(cudaGetLastError());
+  return GSG_OK;
+}
+
+GSG_API int64_t gsg_ctx_launch_count(gsg_ctx_t c) { return c ? c->launches : -1; }
+
+// ------------------------------------------------------------------------------ subgraph
+GSG_API int gsg_subgraph_upload(gsg_ctx_t c, int32_t n, int64_t nnz, const int64_t* h_indptr, const int32_t* h_indices,
+                                const float* h_values, int validate, gsg_subgraph_t* out) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(out, GSG_EINVAL, "out is NULL");
+  *out = nullptr;
+  GSG_CHECK(n >= 0 && nnz >= 0, GSG_EINVAL, "negative n (%d) or nnz (%lld)", n, (long long)nnz);
+  GSG_CHECK(h_indptr && (nnz == 0 || h_indices), GSG_EINVAL, "NULL indptr/indices");
+  if (validate) {
+    if (int rc = validate_csr(n, nnz, h_indptr, h_indices)) return rc;
+  } else {
+    GSG_CHECK(h_indptr[n] == nnz, GSG_EGRAPH, "indptr[n] = %lld != nnz = %lld", (long long)h_indptr[n], (long long)nnz);
+  }
+  DeviceGuard dg(c->device);
+  gsg_subgraph* sg = nullptr;
+  if (int rc = alloc_subgraph(c, n, nnz, h_values != nullptr, &sg)) return rc;
+  int32_t mx = 0;
+  for (int32_t i = 0; i < n; i++) mx = (int32_t)std::max<int64_t>(mx, h_indptr[i + 1] - h_indptr[i]);
+  sg->host_max_deg = mx;
+  cudaError_t e = cudaMemcpyAsync(sg->indptr, h_indptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess && nnz)
+    e = cudaMemcpyAsync(sg->indices, h_indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess && h_values && nnz)
+    e = cudaMemcpyAsync(sg->values, h_values, sizeof(float) * nnz, cudaMemcpyHostToDevice, c->stream);
+  if (e != cudaSuccess) { gsg_subgraph_free(sg); return cuda_fail(e, "cudaMemcpyAsync(upload)"); }
+  *out = sg;
+  return GSG_OK;
+}
+
+GSG_API int gsg_subgraph_upload_device(gsg_ctx_t c, int32_t n, int64_t nnz, const int64_t* d_indptr,
+                                       const int32_t* d_indices, const float* d_values, gsg_subgraph_t* out) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(out, GSG_EINVAL, "out is NULL");
+  *out = nullptr;
+  GSG_CHECK(d_indptr && (nnz == 0 || d_indices), GSG_EINVAL, "NULL indptr/indices");
+  DeviceGuard dg(c->device);
+  gsg_subgraph* sg = nullptr;
+  if (int rc = alloc_subgraph(c, n, nnz, d_values != nullptr, &sg)) return rc;
+  cudaError_t e = cudaMemcpyAsync(sg->indptr, d_indptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, c->stream);
+  if (e == cudaSuccess && nnz)
+    e = cudaMemcpyAsync(sg->indices, d_indices, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, c->stream);
+  if (e == cudaSuccess && d_values && nnz)
+    e = cudaMemcpyAsync(sg->values, d_values, sizeof(float) * nnz, cudaMemcpyDeviceToDevice, c->stream);
+  if (e != cudaSuccess) { gsg_subgraph_free(sg); return cuda_fail(e, "cudaMemcpyAsync(upload_device)"); }
+  *out = sg;
+  return GSG_OK;
+}
+
+GSG_API int gsg_subgraph_normalize(gsg_ctx_t c, gsg_subgraph_t sg, int mode) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
+  DeviceGuard dg(c->device);
+  return normalize_launch(c, sg, mode);
+}
+
+GSG_API int gsg_subgraph_info(gsg_ctx_t c, gsg_subgraph_t sg, int32_t* n, int64_t* nnz_hat, int32_t* max_deg,
+                              int32_t* n_heavy) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
+  DeviceGuard dg(c->device);
+  GSG_CUDA(cudaStreamSynchronize(c->stream));
+  int32_t cnt[2] = {0, 0};
+  if (sg->norm_mode >= 0) GSG_CUDA(cudaMemcpy(cnt, sg->counters + kBins, sizeof(cnt), cudaMemcpyDeviceToHost));
+  if (n) *n = sg->n;
+  if (nnz_hat) *nnz_hat = sg->norm_mode >= 0 ? sg->nnz_hat : -1;
+  if (max_deg) *max_deg = sg->norm_mode >= 0 ? cnt[1] : -1;
+  if (n_heavy) *n_heavy = sg->norm_mode >= 0 ? cnt[0] : -1;
+  return GSG_OK;
+}
+
+GSG_API int gsg_subgraph_download(gsg_ctx_t c, gsg_subgraph_t sg, int64_t* h_indptr, int32_t* h_idx, float* h_val,
+                                  float* h_valT) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(sg && sg->norm_mode >= 0, GSG_EINVAL, "subgraph missing or not normalized");
+  DeviceGuard dg(c->device);
+  GSG_CUDA(cudaStreamSynchronize(c->stream));
+  const int64_t nh = sg->nnz_hat;
+  if (h_indptr) {
+    std::vector<int32_t> tmp(sg->n + 1);
+    GSG_CUDA(cudaMemcpy(tmp.data(), sg->rowptr, sizeof(int32_t) * (sg->n + 1), cudaMemcpyDeviceToHost));
+    for (int32_t i = 0; i <= sg->n; i++) h_indptr[i] = tmp[i];
+  }
+  if (h_idx && nh) GSG_CUDA(cudaMemcpy(h_idx, sg->col, sizeof(int32_t) * nh, cudaMemcpyDeviceToHost));
+  if (h_val && nh) GSG_CUDA(cudaMemcpy(h_val, sg->val, sizeof(float) * nh, cudaMemcpyDeviceToHost));
+  if (h_valT && nh) GSG_CUDA(cudaMemcpy(h_valT, sg->valT, sizeof(float) * nh, cudaMemcpyDeviceToHost));
+  int32_t err = 0;
+  GSG_CUDA(cudaMemcpy(&err, sg->counters + 3 * kBins + 4, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  GSG_CHECK(err == 0, GSG_EGRAPH, "transpose values: a reverse edge was missing (asymmetric structure)");
+  return GSG_OK;
+}
+
+GSG_API int gsg_subgraph_free(gsg_subgraph_t sg) {
+  if (!sg) return GSG_OK;
+  DeviceGuard dg(sg->device);
+  cudaFree(sg->indptr); cudaFree(sg->indices); cudaFree(sg->values);
+  cudaFree(sg->rowptr); cudaFree(sg->col); cudaFree(sg->val); cudaFree(sg->valT);
+  cudaFree(sg->perm); cudaFree(sg->counters);
+  delete sg;
+  return GSG_OK;
+}
+
+// ------------------------------------------------------------------------------ kernels
+GSG_API int gsg_spmm(gsg_ctx_t c, gsg_subgraph_t sg, int transpose, int32_t f, const float* X, int64_t ldx, float* Y,
+                     int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
+  DeviceGuard dg(c->device);
+  return spmm_launch(c, sg, transpose ? 1 : 0, f, X, ldx, Y, ldy, Ylp, ldylp, mask, ldm);
+}
+
+GSG_API int gsg_gemm(gsg_ctx_t c, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int transA, const void* B,
+                     int64_t ldb, int transB, float* C, int64_t ldc, void* Clp, int64_t ldclp, int precision, int epilogue,
+                     const float* aux, int64_t ldaux, int split_k, int accumulate) {
+  if (int rc = check_ctx(c)) return rc;
+  DeviceGuard dg(c->device);
+  return gemm_launch(c, M, N, K, A, lda, transA ? 1 : 0, B, ldb, transB ? 1 : 0, C, ldc, Clp, ldclp, precision,
+                     epilogue, aux, ldaux, split_k, accumulate);
+}
+
+GSG_API int gsg_to_bf16(gsg_ctx_t c, int32_t rows, int32_t cols, const float* src, int64_t lds, void* dst, int64_t ldd) {
+  if (int rc = check_ctx(c)) return rc;
+  DeviceGuard dg(c->device);
+  return to_bf16_launch(c, rows, cols, src, lds, dst, ldd);
+}
+
+GSG_API int gsg_layer_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32_t f_out, const float* X, int64_t ldx,
+                              const float* W, int64_t ldw, float* P, int64_t ldp, void* Plp, int64_t ldplp, float* H,
+                              int64_t ldh, void* Hlp, int64_t ldhlp, int precision, int flags) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
+  GSG_CHECK(f_in >= 1 && f_out >= 1, GSG_EINVAL, "f_in=%d f_out=%d must be >= 1", f_in, f_out);
+  GSG_CHECK(W && ldw >= f_out, GSG_EINVAL, "W NULL or ldw < f_out");
+  GSG_CHECK(precision != GSG_PREC_BF16 || Plp, GSG_EINVAL, "BF16 forward needs the bf16 P copy (Plp)");
+  DeviceGuard dg(c->device);
+  const int n = sg->n;
+  int rc = spmm_launch(c, sg, 0, f_in, X, ldx, P, ldp, precision == GSG_PREC_BF16 ? Plp : nullptr, ldplp, nullptr, 0);
+  if (rc) return rc;
+  const int epi = (flags & GSG_NO_RELU) ? GSG_EPI_NONE : GSG_EPI_RELU;
+  if (precision == GSG_PREC_BF16) {
+    const int64_t ldwl = round_up(f_out, 8);
+    if ((rc = c->ws_lp0.reserve(sizeof(uint16_t) * f_in * ldwl))) return rc;
+    if ((rc = to_bf16_launch(c, f_in, f_out, W, ldw, c->ws_lp0.ptr, ldwl))) return rc;
+    return gemm_launch(c, n, f_out, f_in, Plp, ldplp, 0, c->ws_lp0.ptr, ldwl, 0, H, ldh, Hlp, ldhlp, precision, epi,
+                       nullptr, 0, 0, 0);
+  }
+  return gemm_launch(c, n, f_out, f_in, P, ldp, 0, W, ldw, 0, H, ldh, Hlp, ldhlp, precision, epi, nullptr, 0, 0, 0);
+}
+
+GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32_t f_out, const float* P, int64_t ldp,
+                               const void* Plp, int64_t ldplp, const float* H, int64_t ldh, const float* dH, int64_t lddh,
+                               const void* dHlp, int64_t lddhlp, const float* W, int64_t ldw, float* dW, int64_t lddw,
+                               float* dX, int64_t lddx, void* dXlp, int64_t lddxlp, const float* Hbelow, int64_t ldhb,
+                               int precision, int flags) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
+  GSG_CHECK(f_in >= 1 && f_out >= 1, GSG_EINVAL, "f_in=%d f_out=%d must be >= 1", f_in, f_out);
+  GSG_CHECK(P && dH && W && dW, GSG_EINVAL, "P, dH, W, dW must be non-NULL");
+  GSG_CHECK((flags & GSG_DH_PREMASKED) || H, GSG_EINVAL, "H is needed unless GSG_DH_PREMASKED");
+  GSG_CHECK(precision != GSG_PREC_BF16 || Plp, GSG_EINVAL, "BF16 backward needs the bf16 P copy (Plp)");
+  GSG_CHECK(lddh >= f_out && lddh % 4 == 0, GSG_EINVAL, "lddh must be >= f_out and a multiple of 4");
+  DeviceGuard dg(c->device);
+  const int n = sg->n;
+  const bool bf16 = precision == GSG_PREC_BF16;
+  int rc;
+  // dZ = dH ⊙ 1[H > 0]   (row a4)
+  const float* dZ = dH;
+  int64_t lddz = lddh;
+  const void* dZlp = dHlp;
+  int64_t lddzlp = lddhlp;
+  if (!(flags & GSG_DH_PREMASKED)) {
+    lddz = round_up(f_out, 4);
+    if ((rc = c->ws_dZ.reserve(sizeof(float) * n * lddz))) return rc;
+    void* lp = nullptr;
+    if (bf16) {
+      lddzlp = round_up(f_out, 8);
+      if ((rc = c->ws_lp1.reserve(sizeof(uint16_t) * n * lddzlp))) return rc;
+      lp = c->ws_lp1.ptr;
+    }
+    if ((rc = mask_launch(c, n, f_out, dH, lddh, H, ldh, (float*)c->ws_dZ.ptr, lddz, lp, lddzlp))) return rc;
+    dZ = (const float*)c->ws_dZ.ptr;
+    dZlp = lp;
+  } else if (bf16 && !dZlp) {
+    lddzlp = round_up(f_out, 8);
+    if ((rc = c->ws_lp1.reserve(sizeof(uint16_t) * n * lddzlp))) return rc;
+    if ((rc = to_bf16_launch(c, n, f_out, dH, lddh, c->ws_lp1.ptr, lddzlp))) return rc;
+    dZlp = c->ws_lp1.ptr;
+  }
+  const void* Wop = W;
+  int64_t ldwop = ldw;
+  if (bf16) {
+    ldwop = round_up(f_out, 8);
+    if ((rc = c->ws_lp0.reserve(sizeof(uint16_t) * f_in * ldwop))) return rc;
+    if ((rc = to_bf16_launch(c, f_in, f_out, W, ldw, c->ws_lp0.ptr, ldwop))) return rc;
+    Wop = c->ws_lp0.ptr;
+  }
+  // dW = Pᵀ dZ   (row a5): A = P stored n x f_in (MN-major), B = dZ stored n x f_out (MN-major)
+  rc = gemm_launch(c, f_in, f_out, n, bf16 ? Plp : (const void*)P, bf16 ? ldplp : ldp, 1, bf16 ? dZlp : (const void*)dZ,
+                   bf16 ? lddzlp : lddz, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0,
+                   (flags & GSG_ACCUM_DW) ? 1 : 0);
+  if (rc) return rc;
+  if (!dX) return GSG_OK;
+  // T = dZ Wᵀ   (row a6): A = dZ (K-major), B = W stored f_in x f_out = N x K (K-major)
+  const int64_t ldt = round_up(f_in, 4);
+  if ((rc = c->ws_T.reserve(sizeof(float) * n * ldt))) return rc;
+  float* T = (float*)c->ws_T.ptr;
+  rc = gemm_launch(c, n, f_in, f_out, bf16 ? dZlp : (const void*)dZ, bf16 ? lddzlp : lddz, 0, Wop, ldwop, 1, T, ldt,
+                   nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, 0);
+  if (rc) return rc;
+  // dX = Âᵀ T [⊙ 1[H_below > 0]]   (row a7, fused a4 of the layer below)
+  return spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, dXlp, lddxlp, Hbelow, ldhb);
+}
+
+GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, const float* HL, int64_t ldh,
+                     const float* Wm, int64_t ldw, const void* labels, float* S, float* dS, int64_t lds, float* dWm,
+                     int64_t lddw, float* dHL, int64_t lddh, void* dHlp, int64_t lddhlp, float* loss, int precision) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(kind == GSG_HEAD_SOFTMAX || kind == GSG_HEAD_SIGMOID, GSG_EINVAL, "bad head kind %d", kind);
+  GSG_CHECK(n >= 1 && f >= 1 && C >= 1, GSG_EINVAL, "bad head sizes n=%d f=%d C=%d", n, f, C);
+  GSG_CHECK(HL && Wm && labels && S && dS && dWm && dHL && loss, GSG_EINVAL, "NULL head argument");
+  GSG_CHECK(lds >= C && lds % 4 == 0, GSG_EINVAL, "lds must be >= C and a multiple of 4");
+  (void)precision;  // the head runs in TF32: H_L is fp32 and C is small (SUPPORT)
+  DeviceGuard dg(c->device);
+  int rc = gemm_launch(c, n, C, f, HL, ldh, 0, Wm, ldw, 0, S, lds, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
+  if (rc) return rc;
+  if ((rc = head_loss_launch(c, n, C, kind, S, lds, labels, dS, loss))) return rc;
+  rc = gemm_launch(c, f, C, n, HL, ldh, 1, dS, lds, 0, dWm, lddw, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
+  if (rc) return rc;
+  return gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, GSG_PREC_TF32, GSG_EPI_MASK, HL, ldh, 0, 0);
+}
+
+// ------------------------------------------------------------------------------ NCCL
+GSG_API int gsg_nccl_unique_id(void* out) {
+  GSG_CHECK(out, GSG_EINVAL, "out is NULL");
+  Nccl& N = nccl();
+  GSG_CHECK(N.ok, GSG_ENCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  ncclResult_t r = N.GetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(out, &id, sizeof(id));
+  return GSG_OK;
+}
+
+GSG_API int gsg_nccl_comm_init(gsg_ctx_t c, int nranks, int rank, const void* id128, void** out) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(out && id128 && nranks >= 1 && rank >= 0 && rank < nranks, GSG_EINVAL, "bad comm_init arguments");
+  Nccl& N = nccl();
+  GSG_CHECK(N.ok, GSG_ENCCL, "libnccl.so.2 not loadable");
+  DeviceGuard dg(c->device);
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ncclComm_t comm;
+  ncclResult_t r = N.CommInitRank(&comm, nranks, id, rank);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommInitRank");
+  *out = comm;
+  return GSG_OK;
+}
+
+GSG_API int gsg_nccl_comm_destroy(void* comm) {
+  if (!comm) return GSG_OK;
+  Nccl& N = nccl();
+  GSG_CHECK(N.ok, GSG_ENCCL, "libnccl.so.2 not loadable");
+  ncclResult_t r = N.CommDestroy(static_cast<ncclComm_t>(comm));
+  if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
+  return GSG_OK;
+}
+
+GSG_API int gsg_allreduce_grads(gsg_ctx_t c, void* comm, float* const* bufs, const int64_t* counts, int nbufs,
+                                int average) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(comm && bufs && counts && nbufs >= 0, GSG_EINVAL, "bad allreduce arguments");
+  Nccl& N = nccl();
+  GSG_CHECK(N.ok, GSG_ENCCL, "libnccl.so.2 not loadable");
+  DeviceGuard dg(c->device);
+  ncclResult_t r = N.GroupStart();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+  for (int i = 0; i < nbufs; i++) {
+    if (counts[i] <= 0) continue;
+    r = N.AllReduce(bufs[i], bufs[i], (size_t)counts[i], ncclFloat32, average ? ncclAvg : ncclSum,
+                    static_cast<ncclComm_t>(comm), c->stream);
+    if (r != ncclSuccess) { N.GroupEnd(); return nccl_fail(r, "ncclAllReduce"); }
+  }
+  r = N.GroupEnd();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
+  return GSG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// common.cuh -- shared internals of libgsg.so (context, subgraph, error plumbing).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "gsg.h"
+
+namespace gsg {
+
+constexpr int kHeavyMinDeg = 256;   // deg' >= this -> CTA-cooperative row (degree bin "heavy")
+constexpr int kBins = 32;           // log2 degree buckets
+
+void set_error(const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define GSG_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return ::gsg::cuda_fail(_e, #call); \
+  } while (0)
+
+#define GSG_CHECK(cond, code, ...)                       \
+  do {                                                   \
+    if (!(cond)) return ::gsg::fail(code, __VA_ARGS__);  \
+  } while (0)
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int reserve(size_t b) {
+    if (b <= bytes) return GSG_OK;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    size_t nb = b + b / 4 + 256;
+    cudaError_t e = cudaMalloc(&ptr, nb);
+    if (e != cudaSuccess) { ptr = nullptr; return fail(GSG_ENOMEM, "cudaMalloc(%zu) failed: %s", nb, cudaGetErrorString(e)); }
+    bytes = nb;
+    return GSG_OK;
+  }
+  void release() { if (ptr) cudaFree(ptr); ptr = nullptr; bytes = 0; }
+};
+
+}  // namespace gsg
+
+struct gsg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  int64_t launches = 0;
+  gsg::DevBuf ws_splitk;   // split-K partials
+  gsg::DevBuf ws_T;        // T = dZ Wᵀ (fp32)
+  gsg::DevBuf ws_dZ;       // masked dZ (fp32)
+  gsg::DevBuf ws_lp0;      // bf16 scratch (W copy)
+  gsg::DevBuf ws_lp1;      // bf16 scratch (dZ copy / T copy)
+  gsg::DevBuf ws_lp2;      // bf16 scratch
+  gsg::DevBuf ws_loss;     // per-block loss partials
+};
+
+struct gsg_subgraph {
+  int device = 0;
+  int32_t n = 0;
+  int64_t nnz = 0;          // raw entries (no self loops)
+  int64_t nnz_hat = 0;      // entries of Â (after normalization)
+  int norm_mode = -1;
+  int32_t host_max_deg = -1;
+  // raw structure (device)
+  int64_t* indptr = nullptr;    // [n+1]
+  int32_t* indices = nullptr;   // [nnz]
+  float* values = nullptr;      // [nnz] or null
+  // normalized Â (device)
+  int32_t* rowptr = nullptr;    // [n+1]
+  int32_t* col = nullptr;       // [nnz_hat]
+  float* val = nullptr;         // [nnz_hat]
+  float* valT = nullptr;        // [nnz_hat]
+  int32_t* perm = nullptr;      // [n] rows by descending degree bucket
+  int32_t* counters = nullptr;  // [kBins + 8]: bucket counts ..., [kBins]=n_heavy, [kBins+1]=max_deg
+  size_t cap_hat = 0;
+};
+
+namespace gsg {
+inline void count_launch(gsg_ctx* c, int k = 1) { c->launches += k; }
+
+// launch wrappers implemented in the .cu files
+int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode);
+int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, const float* X, int64_t ldx,
+                float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm);
+int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA,
+                const void* B, int64_t ldb, int transB, float* C, int64_t ldc, void* Clp, int64_t ldclp,
+                int precision, int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate);
+int to_bf16_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t lds, void* dst, int64_t ldd);
+int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh, const float* H, int64_t ldh,
+                float* dZ, int64_t lddz, void* dZlp, int64_t lddzlp);
+int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64_t lds, const void* labels,
+                     float* dS, float* loss);
+}  // namespace gsg

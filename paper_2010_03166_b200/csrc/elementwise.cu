@@ -1,0 +1,131 @@
+// elementwise.cu -- row a4 standalone ReLU' gate (dZ = dH ⊙ 1[H > 0], P:695-707 mask(·),
+// reading R4: ReLU'(0) = 0) for configs whose upstream gradient dH is given, and the
+// classifier-head loss kernel (SUPPORT row a8; Eqs. 2-4, Eq. 9).
+// Everything else elementwise is fused into the SpMM / GEMM epilogues.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace gsg {
+namespace {
+
+__global__ void k_mask(int rows, int cols4, const float4* __restrict__ dH, int64_t lddh4, const float4* __restrict__ H,
+                       int64_t ldh4, float4* __restrict__ dZ, int64_t lddz4, uint2* __restrict__ dZlp, int64_t lddzlp4) {
+  const int64_t total = (int64_t)rows * cols4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / cols4), c = (int)(i % cols4);
+    const float4 g = __ldg(dH + (int64_t)r * lddh4 + c);
+    const float4 h = __ldg(H + (int64_t)r * ldh4 + c);
+    float4 z;
+    z.x = h.x > 0.f ? g.x : 0.f;
+    z.y = h.y > 0.f ? g.y : 0.f;
+    z.z = h.z > 0.f ? g.z : 0.f;
+    z.w = h.w > 0.f ? g.w : 0.f;
+    dZ[(int64_t)r * lddz4 + c] = z;
+    if (dZlp) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(z.x, z.y), hi = __floats2bfloat162_rn(z.z, z.w);
+      uint2 p;
+      p.x = *reinterpret_cast<uint32_t*>(&lo);
+      p.y = *reinterpret_cast<uint32_t*>(&hi);
+      dZlp[(int64_t)r * lddzlp4 + c] = p;
+    }
+  }
+}
+
+constexpr int kHeadThreads = 256;
+constexpr int kHeadBlocks = 256;  // fixed grid -> fixed reduction order (deterministic loss)
+
+// One warp per row. S+ = ReLU(S); Y = softmax(S+) or sigmoid(S+); per-row CE; dS = (Y-Ybar)/n ⊙ 1[S>0].
+__global__ void __launch_bounds__(kHeadThreads) k_head(int n, int C, int kind, const float* __restrict__ S, int64_t lds,
+                                                       const int32_t* __restrict__ cls, const uint8_t* __restrict__ ind,
+                                                       float* __restrict__ dS, float* __restrict__ partial) {
+  __shared__ float wsum[kHeadThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = kHeadThreads / 32;
+  const float inv_n = 1.0f / (float)n;
+  float acc = 0.f;  // this lane's share of the block's loss (fixed order)
+  for (int i = blockIdx.x * nw + warp; i < n; i += gridDim.x * nw) {
+    const float* s = S + (int64_t)i * lds;
+    float* g = dS + (int64_t)i * lds;
+    if (kind == GSG_HEAD_SOFTMAX) {
+      float mx = 0.f;  // S+ >= 0
+      for (int c = lane; c < C; c += 32) mx = fmaxf(mx, fmaxf(s[c], 0.f));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float z = 0.f;
+      for (int c = lane; c < C; c += 32) z += expf(fmaxf(s[c], 0.f) - mx);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+      const float lse = mx + logf(z);
+      const int y = cls[i];
+      for (int c = lane; c < C; c += 32) {
+        const float sv = s[c];
+        const float p = expf(fmaxf(sv, 0.f) - lse);
+        g[c] = sv > 0.f ? (p - (c == y ? 1.f : 0.f)) * inv_n : 0.f;
+      }
+      if (lane == 0) acc += lse - fmaxf(s[y], 0.f);
+    } else {
+      for (int c = lane; c < C; c += 32) {
+        const float sv = s[c];
+        const float sp = fmaxf(sv, 0.f);
+        const float yb = ind[(int64_t)i * C + c] ? 1.f : 0.f;
+        const float p = 1.f / (1.f + expf(-sp));
+        acc += log1pf(expf(-sp)) + sp - yb * sp;
+        g[c] = sv > 0.f ? (p - yb) * inv_n : 0.f;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) wsum[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < nw; w++) t += wsum[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_head_final(int nblocks, int n, const float* __restrict__ partial, float* __restrict__ loss) {
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < nblocks; b++) t += partial[b];
+    *loss = (float)(t / n);
+  }
+}
+
+}  // namespace
+
+int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh, const float* H, int64_t ldh, float* dZ,
+                int64_t lddz, void* dZlp, int64_t lddzlp) {
+  GSG_CHECK(dH && H && dZ, GSG_EINVAL, "mask: NULL argument");
+  GSG_CHECK(lddh % 4 == 0 && ldh % 4 == 0 && lddz % 4 == 0 && (!dZlp || lddzlp % 8 == 0), GSG_EINVAL,
+            "mask: strides must be multiples of 4 (bf16: 8)");
+  if (rows == 0 || cols == 0) return GSG_OK;
+  const int cols4 = (cols + 3) / 4;
+  const int64_t total = (int64_t)rows * cols4;
+  int grid = (int)((total + 255) / 256);
+  if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
+  k_mask<<<grid, 256, 0, ctx->stream>>>(rows, cols4, (const float4*)dH, lddh / 4, (const float4*)H, ldh / 4,
+                                        (float4*)dZ, lddz / 4, (uint2*)dZlp, lddzlp / 4);
+  count_launch(ctx);
+  GSG_CUDA(cudaGetLastError());
+  return GSG_OK;
+}
+
+int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64_t lds, const void* labels, float* dS,
+                     float* loss) {
+  int rc = ctx->ws_loss.reserve(sizeof(float) * kHeadBlocks);
+  if (rc) return rc;
+  float* part = (float*)ctx->ws_loss.ptr;
+  k_head<<<kHeadBlocks, kHeadThreads, 0, ctx->stream>>>(n, C, kind, S, lds,
+                                                        kind == GSG_HEAD_SOFTMAX ? (const int32_t*)labels : nullptr,
+                                                        kind == GSG_HEAD_SIGMOID ? (const uint8_t*)labels : nullptr,
+                                                        dS, part);
+  k_head_final<<<1, 32, 0, ctx->stream>>>(kHeadBlocks, n, part, loss);
+  count_launch(ctx, 2);
+  GSG_CUDA(cudaGetLastError());
+  return GSG_OK;
+}
+
+}  // namespace gsg

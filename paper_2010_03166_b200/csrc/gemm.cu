@@ -1,0 +1,577 @@
+// gemm.cu -- SURVEY §8(a) rows a3 (H = ReLU(P W)), a5 (dW = Pᵀ dZ), a6 (T = dZ Wᵀ) and the
+// head GEMMs: the paper's "weight transformation" (MKL cblas_dgemm at P:1204),
+// re-designed as a warp-specialized tcgen05 kernel for sm_100a:
+//   warp 0        TMA producer  (cp.async.bulk.tensor, 128B swizzle, S-stage smem ring)
+//   warp 1        MMA issuer    (one thread issues tcgen05.mma kind::tf32 / kind::f16,
+//                                M=128, N=BN, accumulators in TMEM)
+//   warp 2        TMEM allocator (2 x BN fp32 accumulator columns: double-buffered tiles)
+//   warps 4..7    epilogue      (tcgen05.ld 32x32b -> ReLU / ReLU'-mask / split-K partial ->
+//                                global stores, optional bf16 copy)
+// Persistent grid over (m-block, n-block, k-split) tiles. Operands are read straight from the
+// row-major activations: K-major (A = P or dZ; B = Wᵀ) or MN-major (A = Pᵀ, B = W or dZ)
+// shared-memory descriptors, so no transposed copies are ever materialized.
+// Split-K partials are reduced in a fixed split order (bitwise reproducible).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace gsg {
+namespace {
+
+constexpr int BM = 128;
+constexpr int kGemmThreads = 256;
+
+// ------------------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+template <bool BF16>
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  if constexpr (BF16) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor (sm_100 version bits). layout: 2 = SWIZZLE_128B (16-byte
+// granules, 8-row atoms), 1 = SWIZZLE_128B_BASE32B (32-byte granules, 4-row atoms) -- the only
+// layout tcgen05 accepts for MN-major 32-bit (tf32) operands.
+template <int LAYOUT = 2>
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | ((uint64_t)LAYOUT << 61);
+}
+
+// MN-major operand descriptor for k-step kk: MN blocks of 128 B at stride BK*128 (LBO);
+// bf16: 8-row SW128 atoms (SBO 1024), tf32: 4-row SW128_BASE32B atoms (SBO 512). One k-step
+// covers UMMA_K rows of 128 B = 1024 B (tf32, 8 rows) or 2048 B (bf16, 16 rows).
+template <bool BF16, int BK>
+__device__ __forceinline__ uint64_t mn_desc(uint32_t base, int kk) {
+  if constexpr (BF16) return smem_desc<2>(base + kk * 2048, BK * 128, 1024);
+  else return smem_desc<1>(base + kk * 1024, BK * 128, 512);
+}
+
+struct GemmArgs {
+  int M, N, K;
+  int num_m, num_n, splits, kb_per_split, num_kb;
+  float* C;
+  int64_t ldc;
+  __nv_bfloat16* Clp;
+  int64_t ldclp;
+  const float* aux;
+  int64_t ldaux;
+  int epi;          // GSG_EPI_*
+  int accumulate;
+  float* ws;        // split-K partials [splits][M][ldws]
+  int64_t ldws;
+  uint32_t idesc;
+};
+
+template <int BN, bool BF16>
+struct Cfg {
+  static constexpr int ELEM = BF16 ? 2 : 4;
+  static constexpr int BK = 128 / ELEM;             // one 128-byte swizzle row of K
+  static constexpr int UMMA_K = 32 / ELEM;          // 8 (tf32) / 16 (bf16)
+  static constexpr int MN_PER_ROW = 128 / ELEM;     // MN elements per 128B row (MN-major)
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN >= 256 ? 4 : 6;
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+};
+
+template <int BN, bool BF16, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs g) {
+  using C = Cfg<BN, BF16>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tiles = g.num_m * g.num_n * g.splits;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < C::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int per_split = g.num_m * g.num_n;
+        const int s = t / per_split, r = t % per_split;
+        const int mb = r / g.num_n, nb = r % g.num_n;
+        const int kb0 = s * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+        for (int kb = kb0; kb < kb1; kb++) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          const int k0 = kb * C::BK;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / C::MN_PER_ROW; j++)
+              tma_load_2d(sa + j * (C::BK * 128), &tmA, &full[stage], mb * BM + j * C::MN_PER_ROW, k0);
+          } else {
+            tma_load_2d(sa, &tmA, &full[stage], k0, mb * BM);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / C::MN_PER_ROW; j++)
+              tma_load_2d(sb + j * (C::BK * 128), &tmB, &full[stage], nb * BN + j * C::MN_PER_ROW, k0);
+          } else {
+            tma_load_2d(sb, &tmB, &full[stage], k0, nb * BN);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int per_split = g.num_m * g.num_n;
+        const int s = t / per_split;
+        const int kb0 = s * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; kb++) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t b_addr = a_addr + C::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < C::BK / C::UMMA_K; kk++) {
+            uint64_t ad, bd;
+            if constexpr (A_MN) ad = mn_desc<BF16, C::BK>(a_addr, kk);
+            else ad = smem_desc<2>(a_addr + kk * 32, 16, 1024);
+            if constexpr (B_MN) bd = mn_desc<BF16, C::BK>(b_addr, kk);
+            else bd = smem_desc<2>(b_addr + kk * 32, 16, 1024);
+            tc_mma<BF16>(tmem_d, ad, bd, g.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int per_split = g.num_m * g.num_n;
+      const int s = t / per_split, r = t % per_split;
+      const int mb = r / g.num_n, nb = r % g.num_n;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * BM + q * 32 + lane;
+      const bool row_ok = row < g.M;
+      for (int c = 0; c < BN / 32; c++) {
+        uint32_t v[32];
+        __syncwarp();
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        const int col0 = nb * BN + c * 32;
+        if (!row_ok || col0 >= g.N) continue;
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) x[i] = __uint_as_float(v[i]);
+        if (g.splits > 1) {
+          float* dst = g.ws + ((int64_t)s * g.M + row) * g.ldws + col0;
+          if (col0 + 32 <= g.N) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
+          } else {
+            
+#pragma unroll
+            for (int i = 0; i < 32; i++) if (col0 + i < g.N) dst[i] = x[i];
+          }
+          continue;
+        }
+        float* dst = g.C + (int64_t)row * g.ldc + col0;
+        const bool full_chunk = col0 + 32 <= g.N;
+        if (g.accumulate) {
+          if (full_chunk) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 o = *reinterpret_cast<const float4*>(dst + i);
+              x[i] += o.x; x[i + 1] += o.y; x[i + 2] += o.z; x[i + 3] += o.w;
+            }
+          } else {
+            
+#pragma unroll
+            for (int i = 0; i < 32; i++) if (col0 + i < g.N) x[i] += dst[i];
+          }
+        }
+        if (g.epi == GSG_EPI_RELU) {
+#pragma unroll
+          for (int i = 0; i < 32; i++) x[i] = fmaxf(x[i], 0.f);
+        } else if (g.epi == GSG_EPI_MASK) {
+          const float* ax = g.aux + (int64_t)row * g.ldaux + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 m = __ldg(reinterpret_cast<const float4*>(ax + i));
+              x[i] = m.x > 0.f ? x[i] : 0.f;
+              x[i + 1] = m.y > 0.f ? x[i + 1] : 0.f;
+              x[i + 2] = m.z > 0.f ? x[i + 2] : 0.f;
+              x[i + 3] = m.w > 0.f ? x[i + 3] : 0.f;
+            }
+          } else {
+            
+#pragma unroll
+            for (int i = 0; i < 32; i++) if (col0 + i < g.N) x[i] = ax[i] > 0.f ? x[i] : 0.f;
+          }
+        }
+        if (full_chunk) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
+        } else {
+          
+#pragma unroll
+            for (int i = 0; i < 32; i++) if (col0 + i < g.N) dst[i] = x[i];
+        }
+        if (g.Clp) {
+          __nv_bfloat16* dl = g.Clp + (int64_t)row * g.ldclp + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              __nv_bfloat162 p0 = __floats2bfloat162_rn(x[i], x[i + 1]);
+              __nv_bfloat162 p1 = __floats2bfloat162_rn(x[i + 2], x[i + 3]);
+              __nv_bfloat162 p2 = __floats2bfloat162_rn(x[i + 4], x[i + 5]);
+              __nv_bfloat162 p3 = __floats2bfloat162_rn(x[i + 6], x[i + 7]);
+              uint4 u;
+              u.x = *reinterpret_cast<uint32_t*>(&p0);
+              u.y = *reinterpret_cast<uint32_t*>(&p1);
+              u.z = *reinterpret_cast<uint32_t*>(&p2);
+              u.w = *reinterpret_cast<uint32_t*>(&p3);
+              *reinterpret_cast<uint4*>(dl + i) = u;
+            }
+          } else {
+            
+#pragma unroll
+            for (int i = 0; i < 32; i++) if (col0 + i < g.N) dl[i] = __float2bfloat16_rn(x[i]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// C = epi(sum_s ws[s]) in a fixed split order (deterministic split-K reduction).
+__global__ void k_splitk_reduce(GemmArgs g) {
+  const int n4 = (g.N + 3) / 4;
+  const int64_t total = (int64_t)g.M * n4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(i / n4);
+    const int c = (int)(i % n4) * 4;
+    float x[4] = {0.f, 0.f, 0.f, 0.f};
+    const int w = min(4, g.N - c);
+    for (int s = 0; s < g.splits; s++) {
+      const float* p = g.ws + ((int64_t)s * g.M + row) * g.ldws + c;
+      if (w == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(p);
+        x[0] += v.x; x[1] += v.y; x[2] += v.z; x[3] += v.w;
+      } else {
+        for (int j = 0; j < w; j++) x[j] += p[j];
+      }
+    }
+    float* dst = g.C + (int64_t)row * g.ldc + c;
+    for (int j = 0; j < w; j++) {
+      float y = x[j];
+      if (g.accumulate) y += dst[j];
+      if (g.epi == GSG_EPI_RELU) y = fmaxf(y, 0.f);
+      else if (g.epi == GSG_EPI_MASK) y = g.aux[(int64_t)row * g.ldaux + c + j] > 0.f ? y : 0.f;
+      dst[j] = y;
+      if (g.Clp) g.Clp[(int64_t)row * g.ldclp + c + j] = __float2bfloat16_rn(y);
+    }
+  }
+}
+
+// K = 0: C = epi(0) (+ C when accumulating)
+__global__ void k_fill_epi(GemmArgs g) {
+  const int64_t total = (int64_t)g.M * g.N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(i / g.N), c = (int)(i % g.N);
+    float y = g.accumulate ? g.C[(int64_t)row * g.ldc + c] : 0.f;
+    if (g.epi == GSG_EPI_RELU) y = fmaxf(y, 0.f);
+    else if (g.epi == GSG_EPI_MASK) y = g.aux[(int64_t)row * g.ldaux + c] > 0.f ? y : 0.f;
+    g.C[(int64_t)row * g.ldc + c] = y;
+    if (g.Clp) g.Clp[(int64_t)row * g.ldclp + c] = __float2bfloat16_rn(y);
+  }
+}
+
+__global__ void k_to_bf16(int rows, int cols, const float* __restrict__ src, int64_t lds, __nv_bfloat16* __restrict__ dst,
+                          int64_t ldd) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / cols), c = (int)(i % cols);
+    dst[(int64_t)r * ldd + c] = __float2bfloat16_rn(src[(int64_t)r * lds + c]);
+  }
+}
+
+// --------------------------------------------------------------------------- host helpers
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+int get_encode() {
+  static std::once_flag once;
+  static int rc = GSG_OK;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) {
+      rc = fail(GSG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+      return;
+    }
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return rc;
+}
+
+// 2-D row-major tensor [rows x cols] (ld elements), box {box_cols, box_rows}, 128B swizzle.
+int make_map(CUtensorMap* m, const void* base, bool bf16, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+             int box_rows, bool mn_major) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * (bf16 ? 2 : 4))};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                        const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        (mn_major && !bf16) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(GSG_EINVAL, "cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld box=%dx%d", (int)r,
+                (long long)rows, (long long)cols, (long long)ld, box_cols, box_rows);
+  return GSG_OK;
+}
+
+template <int BN, bool BF16, bool A_MN, bool B_MN>
+int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& g) {
+  using C = Cfg<BN, BF16>;
+  auto kern = k_gemm<BN, BF16, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    GSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  const int tiles = g.num_m * g.num_n * g.splits;
+  const int grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
+  kern<<<grid, kGemmThreads, C::SMEM, ctx->stream>>>(ma, mb, g);
+  count_launch(ctx);
+  GSG_CUDA(cudaGetLastError());
+  return GSG_OK;
+}
+
+template <int BN, bool BF16>
+int dispatch_major(gsg_ctx* ctx, bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& g) {
+  if (!a_mn && !b_mn) return run_gemm<BN, BF16, false, false>(ctx, ma, mb, g);
+  if (!a_mn && b_mn) return run_gemm<BN, BF16, false, true>(ctx, ma, mb, g);
+  if (a_mn && !b_mn) return run_gemm<BN, BF16, true, false>(ctx, ma, mb, g);
+  return run_gemm<BN, BF16, true, true>(ctx, ma, mb, g);
+}
+
+}  // namespace
+
+int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
+                int transB, float* Cp, int64_t ldc, void* Clp, int64_t ldclp, int precision, int epilogue,
+                const float* aux, int64_t ldaux, int split_k, int accumulate) {
+  GSG_CHECK(precision == GSG_PREC_TF32 || precision == GSG_PREC_BF16, GSG_EINVAL, "bad precision %d", precision);
+  GSG_CHECK(epilogue >= GSG_EPI_NONE && epilogue <= GSG_EPI_MASK, GSG_EINVAL, "bad epilogue %d", epilogue);
+  GSG_CHECK(M >= 0 && N >= 0 && K >= 0, GSG_EINVAL, "negative GEMM dims");
+  GSG_CHECK(!accumulate || epilogue == GSG_EPI_NONE, GSG_EINVAL, "accumulate only with GSG_EPI_NONE");
+  GSG_CHECK(Cp && ldc >= N && ldc % 4 == 0 && (uintptr_t)Cp % 16 == 0, GSG_EINVAL,
+            "C: need ldc >= N, ldc %% 4 == 0, 16B alignment (ldc=%lld N=%d)", (long long)ldc, N);
+  GSG_CHECK(!Clp || (ldclp >= N && ldclp % 8 == 0 && (uintptr_t)Clp % 16 == 0), GSG_EINVAL,
+            "Clp: need ldclp >= N, ldclp %% 8 == 0, 16B alignment");
+  GSG_CHECK(epilogue != GSG_EPI_MASK || (aux && ldaux >= N && ldaux % 4 == 0 && (uintptr_t)aux % 16 == 0),
+            GSG_EINVAL, "EPI_MASK needs aux with ldaux >= N, ldaux %% 4 == 0, 16B alignment");
+  if (M == 0 || N == 0) return GSG_OK;
+  const bool bf16 = precision == GSG_PREC_BF16;
+  const int elem = bf16 ? 2 : 4;
+  GemmArgs g{};
+  g.M = M; g.N = N; g.K = K;
+  g.C = Cp; g.ldc = ldc;
+  g.Clp = reinterpret_cast<__nv_bfloat16*>(Clp); g.ldclp = ldclp;
+  g.aux = aux; g.ldaux = ldaux; g.epi = epilogue; g.accumulate = accumulate;
+  if (K == 0) {
+    k_fill_epi<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(g);
+    count_launch(ctx);
+    GSG_CUDA(cudaGetLastError());
+    return GSG_OK;
+  }
+  GSG_CHECK(A && B, GSG_EINVAL, "A and B must be non-NULL");
+  // stored shapes: A is (transA ? K x M : M x K), B is (transB ? N x K : K x N)
+  const int64_t a_cols = transA ? M : K, b_cols = transB ? K : N;
+  GSG_CHECK(lda >= a_cols && (lda * elem) % 16 == 0 && (uintptr_t)A % 16 == 0, GSG_EINVAL,
+            "A: lda=%lld must be >= %lld with 16-byte rows/alignment", (long long)lda, (long long)a_cols);
+  GSG_CHECK(ldb >= b_cols && (ldb * elem) % 16 == 0 && (uintptr_t)B % 16 == 0, GSG_EINVAL,
+            "B: ldb=%lld must be >= %lld with 16-byte rows/alignment", (long long)ldb, (long long)b_cols);
+  int rc = get_encode();
+  if (rc) return rc;
+  const int BN = N <= 128 ? 128 : 256;
+  const int BK = 128 / elem, mnrow = 128 / elem;
+  g.num_m = (M + BM - 1) / BM;
+  g.num_n = (N + BN - 1) / BN;
+  g.num_kb = (K + BK - 1) / BK;
+  const int base_tiles = g.num_m * g.num_n;
+  int splits = split_k;
+  if (splits <= 0) {
+    splits = 1;
+    if (base_tiles < ctx->num_sms / 2) {
+      splits = ctx->num_sms / base_tiles;
+      int max_s = g.num_kb / 4;  // keep >= 4 k-blocks per split
+      if (splits > max_s) splits = max_s;
+      if (splits < 1) splits = 1;
+    }
+  }
+  if (splits > g.num_kb) splits = g.num_kb;
+  g.kb_per_split = (g.num_kb + splits - 1) / splits;
+  g.splits = (g.num_kb + g.kb_per_split - 1) / g.kb_per_split;  // no empty split
+  if (g.splits > 1) {
+    g.ldws = (N + 3) / 4 * 4;
+    rc = ctx->ws_splitk.reserve((size_t)g.splits * M * g.ldws * sizeof(float));
+    if (rc) return rc;
+    g.ws = static_cast<float*>(ctx->ws_splitk.ptr);
+  }
+  // instruction descriptor: D=F32, A/B = TF32 (2) or BF16 (1), majorness, N>>3, M>>4
+  const uint32_t fmt = bf16 ? 1u : 2u;
+  g.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(transA ? 1 : 0) << 15) |
+            ((uint32_t)(transB ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  CUtensorMap ma, mb;
+  if (transA) rc = make_map(&ma, A, bf16, K, M, lda, mnrow, BK, true);   // MN-major A (stored K x M)
+  else rc = make_map(&ma, A, bf16, M, K, lda, BK, BM, false);            // K-major A (stored M x K)
+  if (rc) return rc;
+  if (transB) rc = make_map(&mb, B, bf16, N, K, ldb, BK, BN, false);     // K-major B (stored N x K)
+  else rc = make_map(&mb, B, bf16, K, N, ldb, mnrow, BK, true);          // MN-major B (stored K x N)
+  if (rc) return rc;
+  const bool a_mn = transA, b_mn = !transB;
+  if (bf16) rc = BN == 128 ? dispatch_major<128, true>(ctx, a_mn, b_mn, ma, mb, g) : dispatch_major<256, true>(ctx, a_mn, b_mn, ma, mb, g);
+  else rc = BN == 128 ? dispatch_major<128, false>(ctx, a_mn, b_mn, ma, mb, g) : dispatch_major<256, false>(ctx, a_mn, b_mn, ma, mb, g);
+  if (rc) return rc;
+  if (g.splits > 1) {
+    int64_t total = (int64_t)M * ((N + 3) / 4);
+    int grid = (int)((total + 255) / 256);
+    if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
+    k_splitk_reduce<<<grid, 256, 0, ctx->stream>>>(g);
+    count_launch(ctx);
+    GSG_CUDA(cudaGetLastError());
+  }
+  return GSG_OK;
+}
+
+int to_bf16_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t lds, void* dst, int64_t ldd) {
+  GSG_CHECK(rows >= 0 && cols >= 0 && lds >= cols && ldd >= cols, GSG_EINVAL, "bad to_bf16 shape");
+  if (rows == 0 || cols == 0) return GSG_OK;
+  int64_t total = (int64_t)rows * cols;
+  int grid = (int)((total + 255) / 256);
+  if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
+  k_to_bf16<<<grid, 256, 0, ctx->stream>>>(rows, cols, src, lds, static_cast<__nv_bfloat16*>(dst), ldd);
+  count_launch(ctx);
+  GSG_CUDA(cudaGetLastError());
+  return GSG_OK;
+}
+
+}  // namespace gsg

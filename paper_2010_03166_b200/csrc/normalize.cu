@@ -1,0 +1,161 @@
+// normalize.cu -- SURVEY §8(a) row a1: build Â (self loops, values), its transposed values
+// (device gather form of Alg. 4) and the degree bins used by the SpMMs.
+// Everything is stream-ordered; no host synchronization.
+#include "common.cuh"
+
+namespace gsg {
+namespace {
+
+__device__ __forceinline__ int bucket_of(int d) { return d <= 0 ? 0 : 32 - __clz(d); }
+
+// rowptr[i] = indptr[i] + self*i ; histogram of degree buckets ; max degree
+__global__ void k_rowptr(int n, const int64_t* __restrict__ indptr, int self, int32_t* __restrict__ rowptr,
+                         int32_t* __restrict__ counters) {
+  __shared__ int hist[kBins];
+  __shared__ int mx;
+  if (threadIdx.x < kBins) hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) mx = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+    rowptr[i] = (int32_t)(indptr[i] + (self ? i : 0));
+    if (i < n) {
+      int d = (int)(indptr[i + 1] - indptr[i]) + self;
+      atomicAdd(&hist[bucket_of(d)], 1);
+      atomicMax(&mx, d);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kBins && hist[threadIdx.x]) atomicAdd(&counters[threadIdx.x], hist[threadIdx.x]);
+  if (threadIdx.x == 0) atomicMax(&counters[kBins + 1], mx);
+}
+
+// One warp per row: copy the neighbor list inserting the self loop at its sorted position and
+// compute the values of the requested normalization in fp64 (rounded once to fp32).
+__global__ void k_fill(int n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                       const float* __restrict__ values, int mode, const int32_t* __restrict__ rowptr,
+                       int32_t* __restrict__ col, float* __restrict__ val) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int self = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_SYM_SELF);
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const int64_t b = indptr[i], e = indptr[i + 1];
+    const int d = (int)(e - b);
+    const int32_t o = rowptr[i];
+    const double di = (double)d;
+    int below = 0;  // neighbors with id < i seen so far
+    for (int64_t k0 = b; k0 < e; k0 += 32) {
+      const int64_t k = k0 + lane;
+      const bool ok = k < e;
+      const int j = ok ? indices[k] : 0x7fffffff;
+      const unsigned lt = __ballot_sync(0xffffffffu, ok && j < i);
+      if (ok) {
+        const int pos = (int)(k - b) + (self && j > i ? 1 : 0);
+        double a;
+        if (mode == GSG_NORM_ROW_SELF) a = 1.0 / (di + 1.0);
+        else if (mode == GSG_NORM_SYM_SELF) a = 1.0 / sqrt((di + 1.0) * ((double)(indptr[j + 1] - indptr[j]) + 1.0));
+        else if (mode == GSG_NORM_ROW) a = 1.0 / di;
+        else a = (double)values[k];
+        col[o + pos] = j;
+        val[o + pos] = (float)a;
+      }
+      below += __popc(lt);
+    }
+    if (self && lane == 0) {
+      col[o + below] = i;
+      val[o + below] = (float)(1.0 / (di + 1.0));
+    }
+  }
+}
+
+// valT at slot (u, v) = val at slot (v, u): binary search for u in row v's ascending list.
+// One warp per row u. This reproduces Alg. 4's DataTrans exactly (same structure, a pure
+// permutation of val).
+__global__ void k_transpose_vals(int n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                 const float* __restrict__ val, float* __restrict__ valT, int32_t* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
+    const int b = rowptr[u], e = rowptr[u + 1];
+    for (int k = b + lane; k < e; k += 32) {
+      const int v = col[k];
+      int lo = rowptr[v], hi = rowptr[v + 1] - 1;
+      int found = -1;
+      while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        const int c = col[mid];
+        if (c == u) { found = mid; break; }
+        if (c < u) lo = mid + 1; else hi = mid - 1;
+      }
+      if (found < 0) { atomicExch(err, 1); valT[k] = __int_as_float(0x7fc00000); }
+      else valT[k] = val[found];
+    }
+  }
+}
+
+// Exclusive offsets of the buckets in DESCENDING bucket order; n_heavy = rows with
+// deg' >= kHeavyMinDeg (buckets >= bucket_of(kHeavyMinDeg)).
+__global__ void k_bin_offsets(int32_t* counters) {
+  if (threadIdx.x == 0) {
+    int acc = 0, heavy = 0;
+    const int hb = 32 - __clz(kHeavyMinDeg);
+    for (int b = kBins - 1; b >= 0; b--) {
+      counters[kBins + 2 + b] = acc;  // cursor start
+      acc += counters[b];
+      if (b >= hb) heavy += counters[b];
+    }
+    counters[kBins] = heavy;
+  }
+}
+
+__global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t* __restrict__ counters,
+                              int32_t* __restrict__ perm) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int d = rowptr[i + 1] - rowptr[i];
+    const int pos = atomicAdd(&counters[kBins + 2 + bucket_of(d)], 1);
+    perm[pos] = i;
+  }
+}
+
+}  // namespace
+
+int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
+  GSG_CHECK(mode >= GSG_NORM_ROW_SELF && mode <= GSG_NORM_VALUES, GSG_EINVAL, "bad norm_mode %d", mode);
+  GSG_CHECK(mode != GSG_NORM_VALUES || sg->values, GSG_EINVAL, "GSG_NORM_VALUES needs uploaded edge values");
+  const int self = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_SYM_SELF);
+  const int64_t nh = sg->nnz + (self ? sg->n : 0);
+  GSG_CHECK(nh < (int64_t)INT32_MAX, GSG_EUNSUPPORTED, "nnz_hat %lld exceeds int32", (long long)nh);
+  const int n = sg->n;
+  cudaStream_t st = ctx->stream;
+  if ((size_t)nh > sg->cap_hat) {
+    cudaFree(sg->col); cudaFree(sg->val); cudaFree(sg->valT);
+    sg->col = nullptr; sg->val = sg->valT = nullptr;
+    size_t c = (size_t)(nh > 0 ? nh : 1);
+    GSG_CUDA(cudaMalloc(&sg->col, c * sizeof(int32_t)));
+    GSG_CUDA(cudaMalloc(&sg->val, c * sizeof(float)));
+    GSG_CUDA(cudaMalloc(&sg->valT, c * sizeof(float)));
+    sg->cap_hat = c;
+  }
+  sg->nnz_hat = nh;
+  sg->norm_mode = mode;
+  GSG_CUDA(cudaMemsetAsync(sg->counters, 0, sizeof(int32_t) * (3 * kBins + 8), st));
+  const int T = 256;
+  int grid = (n + 1 + T - 1) / T;
+  if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
+  if (grid < 1) grid = 1;
+  k_rowptr<<<grid, T, 0, st>>>(n, sg->indptr, self, sg->rowptr, sg->counters);
+  if (n > 0) {
+    int wgrid = (int)(((int64_t)n * 32 + T - 1) / T);
+    if (wgrid > ctx->num_sms * 16) wgrid = ctx->num_sms * 16;
+    k_fill<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->indices, sg->values, mode, sg->rowptr, sg->col, sg->val);
+    k_transpose_vals<<<wgrid, T, 0, st>>>(n, sg->rowptr, sg->col, sg->val, sg->valT, sg->counters + 3 * kBins + 4);
+    k_bin_offsets<<<1, 32, 0, st>>>(sg->counters);
+    k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm);
+    count_launch(ctx, 5);
+  } else {
+    count_launch(ctx, 1);
+  }
+  GSG_CUDA(cudaGetLastError());
+  return GSG_OK;
+}
+
+}  // namespace gsg

@@ -1,0 +1,314 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element.
+
+Tolerances (BASELINE.json north_star; SURVEY §8(c) "GPU vs oracle"):
+  * fp32 SpMM outputs (P = Â X, dX = Âᵀ T):      max|gpu - orc| / max|orc| <= 1e-5
+  * TF32 / BF16 tensor-core GEMM outputs:        max|gpu - orc| / max|orc| <= 5e-3
+  * integer / index work (Â structure, bins):    bit-exact; valT = Alg. 4 permutation of val, bit-exact
+Stage-isolated: each GPU stage is compared with the oracle's stage fed the GPU's own inputs.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+import paper_2010_03166_b200 as gsg
+import workload as wl
+
+pytestmark = pytest.mark.gpu
+
+SPMM_TOL = 1e-5
+GEMM_TOL = 5e-3
+
+
+def rel_err(gpu, ref):
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert gpu.shape == ref.shape, (gpu.shape, ref.shape)
+    assert np.all(np.isfinite(gpu)), "non-finite GPU output"
+    den = np.abs(ref).max()
+    return float(np.abs(gpu - ref).max() / (den if den > 0 else 1.0))
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = gsg.Context(0)
+    yield c
+    c.close()
+
+
+def dev(a: np.ndarray, ld: int | None = None, pad_nan: bool = True):
+    """Row-major device copy with row stride ld (padding filled with NaN to catch leaks)."""
+    a = np.ascontiguousarray(a, np.float32)
+    r, f = a.shape
+    ld = wl.ld_for(f) if ld is None else ld
+    t = torch.full((r, ld), float("nan") if pad_nan else 0.0, dtype=torch.float32, device="cuda")
+    t[:, :f] = torch.from_numpy(a).cuda()
+    return t[:, :f]
+
+
+def empty(r, f, ld=None):
+    ld = wl.ld_for(f) if ld is None else ld
+    return torch.full((r, ld), float("nan"), dtype=torch.float32, device="cuda")[:, :f]
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def graph(n_parent, deg, n, m, seed):
+    p = wl.Parent(n_parent, deg, 2.1, 0.0, seed=seed)
+    return p.frontier_sample(n, m, seed + 1, clip=1)
+
+
+def star_plus_random(n, hub_deg, seed):
+    """A graph with one hub of degree hub_deg (heavy row path) plus random sparse edges."""
+    rng = np.random.default_rng(seed)
+    E = set()
+    for j in rng.choice(np.arange(1, n), size=hub_deg, replace=False):
+        E.add((0, int(j))); E.add((int(j), 0))
+    for _ in range(3 * n):
+        a, b = rng.integers(1, n, 2)
+        if a != b:
+            E.add((int(a), int(b))); E.add((int(b), int(a)))
+    E = sorted(E)
+    ip = np.zeros(n + 1, np.int64)
+    for a, _ in E:
+        ip[a + 1] += 1
+    ip = np.cumsum(ip)
+    ix = np.array([b for _, b in E], np.int32)
+    return wl.CSR(ip, ix)
+
+
+# ------------------------------------------------------------------------------ a1
+@pytest.mark.parametrize("mode", [gsg.GSG_NORM_ROW_SELF, gsg.GSG_NORM_SYM_SELF, gsg.GSG_NORM_ROW, gsg.GSG_NORM_VALUES])
+def test_normalize_matches_oracle(ctx, mode):
+    g = graph(3000, 10.0, 700, 60, 1)
+    vals = wl.random_values(g, 5) if mode == gsg.GSG_NORM_VALUES else None
+    sg = ctx.upload(g.indptr, g.indices, vals).normalize(mode)
+    ip, ix, v, vt = sg.download()
+    A = orc.normalize(g.indptr, g.indices, mode, vals)
+    assert np.array_equal(ip, A.indptr) and np.array_equal(ix, A.idx)  # structure: bit-exact
+    np.testing.assert_allclose(v, A.val, rtol=2 ** -23, atol=0)           # one fp32 rounding
+    # valT must be exactly Alg. 4's DataTrans of the GPU's own values (a permutation)
+    ref_t = orc.transpose_alg4(orc.AHat(ip, ix, v.astype(np.float64)))
+    assert np.array_equal(vt.astype(np.float64), ref_t)
+    inf = sg.info()
+    d = np.diff(ip)
+    assert inf["nnz_hat"] == A.val.size and inf["max_deg_hat"] == d.max()
+    assert inf["n_heavy"] == int((d >= 256).sum())
+
+
+def test_upload_validation(ctx):
+    ok = wl.CSR(np.array([0, 1, 2], np.int64), np.array([1, 0], np.int32))
+    ctx.upload(ok.indptr, ok.indices).free()
+    bad = [
+        (np.array([0, 1, 1], np.int64), np.array([1], np.int32), "not symmetric"),
+        (np.array([0, 1, 2], np.int64), np.array([0, 1], np.int32), "self loop"),
+        (np.array([0, 1, 2], np.int64), np.array([5, 0], np.int32), "out of range"),
+        (np.array([0, 2, 4, 6], np.int64), np.array([2, 1, 0, 2, 0, 1], np.int32), "ascending"),
+    ]
+    for ip, ix, msg in bad:
+        with pytest.raises(gsg.GsgError) as e:
+            ctx.upload(ip, ix)
+        assert e.value.code == gsg.GSG_EGRAPH and msg in str(e.value), str(e.value)
+
+
+# ------------------------------------------------------------------------------ a2 / a7
+@pytest.mark.parametrize("f", [1, 3, 13, 50, 64, 128, 200, 300, 602])
+def test_spmm_forward_and_transpose(ctx, f):
+    g = graph(4000, 12.0, 900, 80, 2)
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW_SELF)
+    sg = ctx.upload(g.indptr, g.indices).normalize(gsg.GSG_NORM_ROW_SELF)
+    rng = np.random.default_rng(f)
+    X = rng.standard_normal((g.n, f)).astype(np.float32)
+    Xd, Y = dev(X), empty(g.n, f)
+    ctx.spmm(sg, Xd, Y)
+    assert rel_err(host(Y), orc.spmm(A, X)) <= SPMM_TOL
+    Yt = empty(g.n, f)
+    ctx.spmm(sg, Xd, Yt, transpose=True)
+    assert rel_err(host(Yt), orc.spmm_t(A, X)) <= SPMM_TOL
+
+
+def test_spmm_heavy_rows_and_mask(ctx):
+    g = star_plus_random(3000, 2500, 3)  # hub degree 2500 -> CTA-split heavy row
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_SYM_SELF)
+    sg = ctx.upload(g.indptr, g.indices).normalize(gsg.GSG_NORM_SYM_SELF)
+    assert sg.info()["n_heavy"] >= 1
+    rng = np.random.default_rng(4)
+    for f in (8, 200, 1024):
+        X = rng.standard_normal((g.n, f)).astype(np.float32)
+        Hb = rng.standard_normal((g.n, f)).astype(np.float32)
+        Y, Ylp = empty(g.n, f), torch.zeros((g.n, wl.ld_for(f, 8)), dtype=torch.bfloat16, device="cuda")[:, :f]
+        ctx.spmm(sg, dev(X), Y, transpose=True, mask=dev(Hb), Ylp=Ylp)
+        ref = np.where(Hb > 0, orc.spmm_t(A, X), 0.0)
+        assert rel_err(host(Y), ref) <= SPMM_TOL
+        yl = host(Ylp)
+        assert np.array_equal(yl, torch.from_numpy(host(Y).astype(np.float32)).bfloat16().float().numpy())
+
+
+def test_spmm_deterministic_and_identity(ctx):
+    g = graph(5000, 20.0, 1500, 100, 5)
+    sg = ctx.upload(g.indptr, g.indices).normalize()
+    X = dev(np.random.default_rng(6).standard_normal((g.n, 256)).astype(np.float32))
+    Y1, Y2 = empty(g.n, 256), empty(g.n, 256)
+    ctx.spmm(sg, X, Y1)
+    ctx.spmm(sg, X, Y2)
+    assert torch.equal(Y1, Y2)
+    # no edges: Â = I -> P = X exactly
+    n = 37
+    e = ctx.upload(np.zeros(n + 1, np.int64), np.zeros(0, np.int32)).normalize()
+    Xi = np.random.default_rng(7).standard_normal((n, 20)).astype(np.float32)
+    Yi = empty(n, 20)
+    ctx.spmm(e, dev(Xi), Yi)
+    assert np.array_equal(host(Yi), Xi.astype(np.float64))
+
+
+# ------------------------------------------------------------------------------ GEMMs
+GEMM_SHAPES = [(128, 128, 32), (300, 200, 50), (1000, 512, 602), (130, 17, 5), (602, 512, 3000), (64, 1024, 1024),
+               (2000, 107, 1024)]
+
+
+@pytest.mark.parametrize("prec", [gsg.GSG_PREC_TF32, gsg.GSG_PREC_BF16])
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_vs_oracle(ctx, prec, ta, tb, M, N, K):
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    ref = orc.gemm(A, B, ta, tb)
+    if prec == gsg.GSG_PREC_BF16:
+        Ad = torch.from_numpy(A).cuda().bfloat16()
+        Bd = torch.from_numpy(B).cuda().bfloat16()
+        pa = torch.zeros((A.shape[0], wl.ld_for(A.shape[1], 8)), dtype=torch.bfloat16, device="cuda")
+        pb = torch.zeros((B.shape[0], wl.ld_for(B.shape[1], 8)), dtype=torch.bfloat16, device="cuda")
+        pa[:, :A.shape[1]] = Ad
+        pb[:, :B.shape[1]] = Bd
+        Ad, Bd = pa[:, :A.shape[1]], pb[:, :B.shape[1]]
+    else:
+        Ad, Bd = dev(A), dev(B)
+    C = empty(M, N)
+    ctx.gemm(Ad, Bd, C, transA=ta, transB=tb, precision=prec, K=K)
+    assert rel_err(host(C), ref) <= GEMM_TOL
+
+
+@pytest.mark.parametrize("split", [1, 3, 7])
+def test_gemm_epilogues_and_splitk(ctx, split):
+    rng = np.random.default_rng(11)
+    M, N, K = 700, 300, 900
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    aux = rng.standard_normal((M, N)).astype(np.float32)
+    ref = orc.gemm(A, B)
+    C = empty(M, N)
+    Clp = torch.zeros((M, wl.ld_for(N, 8)), dtype=torch.bfloat16, device="cuda")[:, :N]
+    ctx.gemm(dev(A), dev(B), C, epilogue=gsg.GSG_EPI_RELU, Clp=Clp, split_k=split)
+    assert rel_err(host(C), np.maximum(ref, 0)) <= GEMM_TOL
+    assert np.array_equal(host(Clp), torch.from_numpy(host(C).astype(np.float32)).bfloat16().float().numpy())
+    ctx.gemm(dev(A), dev(B), C, epilogue=gsg.GSG_EPI_MASK, aux=dev(aux), split_k=split)
+    assert rel_err(host(C), np.where(aux > 0, ref, 0)) <= GEMM_TOL
+    C0 = rng.standard_normal((M, N)).astype(np.float32)
+    Cd = dev(C0)
+    ctx.gemm(dev(A), dev(B), Cd, accumulate=True, split_k=split)
+    assert rel_err(host(Cd), ref + C0) <= GEMM_TOL
+    # bitwise reproducible
+    C1, C2 = empty(M, N), empty(M, N)
+    ctx.gemm(dev(A), dev(B), C1, split_k=split)
+    ctx.gemm(dev(A), dev(B), C2, split_k=split)
+    assert torch.equal(C1, C2)
+
+
+def test_gemm_k0(ctx):
+    C = dev(np.ones((5, 6), np.float32))
+    A = empty(5, 4)
+    ctx.gemm(A, A, C, K=0, M=5, N=6)
+    assert not host(C).any()
+
+
+# ------------------------------------------------------------------------------ layer
+def run_layer(ctx, g, X, W, dH, prec, mode=gsg.GSG_NORM_ROW_SELF, Hb=None):
+    n, fi = X.shape
+    fo = W.shape[1]
+    sg = ctx.upload(g.indptr, g.indices).normalize(mode)
+    Xd, Wd = dev(X), dev(W)
+    P, H = empty(n, fi), empty(n, fo)
+    Plp = torch.zeros((n, wl.ld_for(fi, 8)), dtype=torch.bfloat16, device="cuda")[:, :fi] if prec else None
+    ctx.layer_forward(sg, Xd, Wd, P, H, fi, fo, precision=prec, Plp=Plp)
+    dW, dX = empty(fi, fo), empty(n, fi)
+    ctx.layer_backward(sg, P, H, dev(dH), Wd, dW, dX, fi, fo, precision=prec, Plp=Plp,
+                       H_below=None if Hb is None else dev(Hb))
+    return {k: host(v) for k, v in dict(P=P, H=H, dW=dW, dX=dX).items()}
+
+
+@pytest.mark.parametrize("prec", [gsg.GSG_PREC_TF32, gsg.GSG_PREC_BF16])
+def test_layer_stage_isolated(ctx, prec):
+    cfg = wl.CONFIGS[1]
+    g = wl.sample_subgraph(cfg)
+    inp = wl.make_inputs(cfg, g.n)
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW_SELF)
+    Hb = np.random.default_rng(3).standard_normal(inp.X.shape).astype(np.float32)
+    out = run_layer(ctx, g, inp.X, inp.Ws[0], inp.dH, prec, Hb=Hb)
+    assert rel_err(out["P"], orc.spmm(A, inp.X)) <= SPMM_TOL                       # a2
+    assert rel_err(out["H"], np.maximum(orc.gemm(out["P"], inp.Ws[0]), 0)) <= GEMM_TOL   # a3 (GPU's P)
+    dZ = orc.relu_mask(inp.dH, out["H"])                                            # a4 (GPU's H)
+    assert rel_err(out["dW"], orc.gemm(out["P"], dZ, transA=True)) <= GEMM_TOL     # a5
+    T = orc.gemm(dZ, inp.Ws[0], transB=True)                                        # a6 (oracle)
+    assert rel_err(out["dX"], np.where(Hb > 0, orc.spmm_t(A, T), 0)) <= GEMM_TOL    # a7 after a TF32 GEMM
+
+
+def test_layer_end_to_end_config1(ctx):
+    cfg = wl.CONFIGS[1]
+    g = wl.sample_subgraph(cfg)
+    inp = wl.make_inputs(cfg, g.n)
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW_SELF)
+    out = run_layer(ctx, g, inp.X, inp.Ws[0], inp.dH, gsg.GSG_PREC_TF32)
+    P, Z, H = orc.layer_forward(A, inp.X, inp.Ws[0])
+    assert rel_err(out["H"], H) <= GEMM_TOL
+    # End to end (oracle from the initial inputs), the ReLU' gate may flip only where the TF32
+    # pre-activation error can change the sign: |Z| within the GEMM tolerance of zero.
+    flips = (out["H"] > 0) != (Z > 0)
+    assert np.all(np.abs(Z[flips]) <= GEMM_TOL * np.abs(Z).max())
+    assert flips.mean() < 1e-3
+    # With the gate taken from the GPU's H (the only discontinuity), dW and dX agree at the
+    # GEMM tolerance; each flipped gate moves dW by one P[k,i]*dH[k,j] term (not graded).
+    dZ, dW, T, dX = orc.layer_backward(A, P, Z, np.where(out["H"] > 0, inp.dH, 0.0), inp.Ws[0], premasked=True)
+    assert rel_err(out["dW"], dW) <= GEMM_TOL
+    assert rel_err(out["dX"], dX) <= GEMM_TOL
+
+
+@pytest.mark.parametrize("kind,C", [("softmax", 41), ("sigmoid", 107)])
+def test_head_stage_isolated(ctx, kind, C):
+    rng = np.random.default_rng(8)
+    n, f = 1500, 200
+    HL = np.maximum(rng.standard_normal((n, f)), 0).astype(np.float32)
+    Wm = wl.glorot(rng, f, C) * 8
+    labels = rng.integers(0, C, n).astype(np.int32) if kind == "softmax" else (rng.random((n, C)) < 0.05).astype(np.uint8)
+    lab = torch.from_numpy(labels).cuda()
+    S, dS = empty(n, C), empty(n, C)
+    ldS = S.stride(0)
+    dS = torch.full((n, ldS), float("nan"), device="cuda")[:, :C]
+    dWm, dHL = empty(f, C), empty(n, f)
+    loss = torch.zeros(1, device="cuda")
+    HLd = dev(HL)
+    ctx.head(HLd, dev(Wm), lab, S, dS, dWm, dHL, n, f, C,
+             gsg.GSG_HEAD_SOFTMAX if kind == "softmax" else gsg.GSG_HEAD_SIGMOID, loss)
+    Sg = host(S)
+    assert rel_err(Sg, orc.gemm(HL, Wm)) <= GEMM_TOL
+    l_ref, Y, dS_ref = orc.head(Sg, labels, kind)           # oracle fed the GPU's S
+    assert abs(float(host(loss)[0]) - l_ref) <= 1e-5 * abs(l_ref)
+    assert rel_err(host(dS), dS_ref) <= 1e-5
+    dSg = host(dS)
+    assert rel_err(host(dWm), orc.gemm(HL, dSg, transA=True)) <= GEMM_TOL
+    assert rel_err(host(dHL), np.where(HL > 0, orc.gemm(dSg, Wm, transB=True), 0)) <= GEMM_TOL
+
+
+def test_allreduce_single_rank(ctx):
+    uid = ctx.nccl_unique_id()
+    comm = ctx.nccl_comm_init(1, 0, uid)
+    a = torch.arange(1000, dtype=torch.float32, device="cuda")
+    b = torch.ones(77, dtype=torch.float32, device="cuda")
+    ref_a, ref_b = a.clone(), b.clone()
+    ctx.allreduce_grads(comm, [a, b], average=True)
+    ctx.sync()
+    assert torch.equal(a, ref_a) and torch.equal(b, ref_b)
+    ctx.nccl_comm_destroy(comm)
