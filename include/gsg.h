@@ -104,6 +104,16 @@ GSG_API void* gsg_ctx_stream(gsg_ctx_t ctx);
 GSG_API int gsg_ctx_sync(gsg_ctx_t ctx);
 /* Number of kernels this context has launched so far (evidence counter for benches). */
 GSG_API int64_t gsg_ctx_launch_count(gsg_ctx_t ctx);
+/* Kernel-class profiling (bench evidence): while enabled, every launch of the class is
+ * bracketed by CUDA events on the context stream, and the library accumulates the class's
+ * ALGORITHMIC work: SpMM effective bytes 4*nnz_hat*f + 8*nnz_hat + 4*(n+1)
+ * + 4*n*f per launch; GEMM flops 2*M*N*K. Classes: GSG_K_SPMM, GSG_K_GEMM, GSG_K_NORM,
+ * GSG_K_OTHER. gsg_ctx_profile_read synchronizes the stream, returns the totals since the
+ * last read and resets them. Enabling allocates events lazily (do it outside graph capture). */
+enum { GSG_K_SPMM = 0, GSG_K_GEMM = 1, GSG_K_NORM = 2, GSG_K_OTHER = 3, GSG_K_CLASSES = 4 };
+GSG_API int gsg_ctx_profile(gsg_ctx_t ctx, int enable);
+GSG_API int gsg_ctx_profile_read(gsg_ctx_t ctx, int kclass, double* total_ms, int64_t* launches,
+                                 double* alg_bytes, double* alg_flops);
 /* Thread-local message of the last failing call on this thread ("" if none). */
 GSG_API const char* gsg_last_error(void);
 
@@ -125,6 +135,12 @@ GSG_API const char* gsg_last_error(void);
 GSG_API int gsg_subgraph_upload(gsg_ctx_t ctx, int32_t n, int64_t nnz, const int64_t* h_indptr,
                                 const int32_t* h_indices, const float* h_values, int validate,
                                 gsg_subgraph_t* out);
+/* Refill an existing subgraph with a new host CSR (same contract as gsg_subgraph_upload),
+ * reusing its device arrays when they are large enough (no allocation in the steady state;
+ * copies are asynchronous from pinned host memory). The subgraph must be normalized again. */
+GSG_API int gsg_subgraph_assign(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t n, int64_t nnz,
+                                const int64_t* h_indptr, const int32_t* h_indices,
+                                const float* h_values, int validate);
 /* Same, from DEVICE arrays already resident in HBM (stream-ordered device-to-device copy;
  * no validation). Used when a pool of subgraphs lives on the GPU (Alg. 7 pool). */
 GSG_API int gsg_subgraph_upload_device(gsg_ctx_t ctx, int32_t n, int64_t nnz,

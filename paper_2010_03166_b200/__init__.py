@@ -31,6 +31,7 @@ GSG_PREC_TF32, GSG_PREC_BF16 = 0, 1
 GSG_NO_RELU, GSG_DH_PREMASKED, GSG_ACCUM_DW = 1, 2, 4
 GSG_EPI_NONE, GSG_EPI_RELU, GSG_EPI_MASK = 0, 1, 2
 GSG_HEAD_SOFTMAX, GSG_HEAD_SIGMOID = 0, 1
+GSG_K_SPMM, GSG_K_GEMM, GSG_K_NORM, GSG_K_OTHER = 0, 1, 2, 3
 
 _vp, _i32, _i64, _int = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int
 _SIGS = {
@@ -41,6 +42,10 @@ _SIGS = {
     "gsg_ctx_sync": (_int, [_vp]),
     "gsg_ctx_launch_count": (_i64, [_vp]),
     "gsg_last_error": (ctypes.c_char_p, []),
+    "gsg_ctx_profile": (_int, [_vp, _int]),
+    "gsg_ctx_profile_read": (_int, [_vp, _int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
+                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "gsg_subgraph_assign": (_int, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _int]),
     "gsg_subgraph_upload": (_int, [_vp, _i32, _i64, _vp, _vp, _vp, _int, ctypes.POINTER(_vp)]),
     "gsg_subgraph_upload_device": (_int, [_vp, _i32, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)]),
     "gsg_subgraph_normalize": (_int, [_vp, _vp, _int]),
@@ -133,6 +138,13 @@ class Subgraph:
         check(gsg_subgraph_download(self.ctx.h, self.h, ip.ctypes.data, ix.ctypes.data, v.ctypes.data, vt.ctypes.data))
         return ip, ix[:nh], v[:nh], vt[:nh]
 
+    def assign(self, n: int, nnz: int, indptr_ptr: int, indices_ptr: int, values_ptr: int = 0, validate=False):
+        """Refill from host arrays given as raw pointers (pinned memory -> async copies)."""
+        check(gsg_subgraph_assign(self.ctx.h, self.h, n, nnz, indptr_ptr, indices_ptr or None, values_ptr or None,
+                                  int(validate)))
+        self.n, self.nnz = n, nnz
+        return self
+
     def free(self):
         if self.h:
             gsg_subgraph_free(self.h)
@@ -172,6 +184,14 @@ class Context:
 
     def launch_count(self) -> int:
         return int(gsg_ctx_launch_count(self.h))
+
+    def profile(self, enable: bool = True):
+        check(gsg_ctx_profile(self.h, int(enable)))
+
+    def profile_read(self, kclass: int) -> dict:
+        ms, n, b, f = ctypes.c_double(), _i64(), ctypes.c_double(), ctypes.c_double()
+        check(gsg_ctx_profile_read(self.h, kclass, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b), ctypes.byref(f)))
+        return {"ms": ms.value, "launches": n.value, "alg_bytes": b.value, "alg_flops": f.value}
 
     def close(self):
         if getattr(self, "h", None):

@@ -92,6 +92,9 @@ int alloc_subgraph(gsg_ctx* ctx, int32_t n, int64_t nnz, bool has_values, gsg_su
   sg->device = ctx->device;
   sg->n = n;
   sg->nnz = nnz;
+  sg->cap_n = n;
+  sg->cap_nnz = nnz;
+  sg->has_values = has_values;
   cudaError_t e = cudaSuccess;
   auto A = [&](void** p, size_t b) { if (e == cudaSuccess) e = cudaMalloc(p, b > 0 ? b : 16); };
   A((void**)&sg->indptr, sizeof(int64_t) * (n + 1));
@@ -180,14 +183,14 @@ GSG_API int gsg_ctx_destroy(gsg_ctx_t c) {
   cudaStreamSynchronize(c->stream);
   c->ws_splitk.release(); c->ws_T.release(); c->ws_dZ.release();
   c->ws_lp0.release(); c->ws_lp1.release(); c->ws_lp2.release(); c->ws_loss.release();
-  if (c->own_stream) cudaStreamDestroy(c->stream);
+  for (auto& r : c->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : c->prof.free_ev) cudaEventDestroy(e);
   delete c;
   return GSG_OK;
 }
 
 GSG_API int gsg_ctx_set_stream(gsg_ctx_t c, void* s) {
   if (int rc = check_ctx(c)) return rc;
-  if (c->own_stream) { cudaStreamDestroy(c->stream); c->own_stream = false; }
   c->stream = static_cast<cudaStream_t>(s);
   return GSG_OK;
 }
@@ -203,6 +206,39 @@ GSG_API int gsg_ctx_sync(gsg_ctx_t c) {
 }
 
 GSG_API int64_t gsg_ctx_launch_count(gsg_ctx_t c) { return c ? c->launches : -1; }
+
+GSG_API int gsg_ctx_profile(gsg_ctx_t c, int enable) {
+  if (int rc = check_ctx(c)) return rc;
+  c->prof.on = enable != 0;
+  return GSG_OK;
+}
+
+GSG_API int gsg_ctx_profile_read(gsg_ctx_t c, int kclass, double* total_ms, int64_t* launches, double* alg_bytes,
+                                 double* alg_flops) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(kclass >= 0 && kclass < GSG_K_CLASSES, GSG_EINVAL, "bad kernel class %d", kclass);
+  DeviceGuard dg(c->device);
+  GSG_CUDA(cudaStreamSynchronize(c->stream));
+  double ms = 0.0;
+  int64_t cnt = 0;
+  std::vector<gsg::Profiler::Rec> keep;
+  for (auto& r : c->prof.recs) {
+    if (r.cls != kclass) { keep.push_back(r); continue; }
+    float t = 0.f;
+    GSG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms += t;
+    cnt++;
+    c->prof.free_ev.push_back(r.a);
+    c->prof.free_ev.push_back(r.b);
+  }
+  c->prof.recs.swap(keep);
+  if (total_ms) *total_ms = ms;
+  if (launches) *launches = cnt;
+  if (alg_bytes) *alg_bytes = c->prof.bytes[kclass];
+  if (alg_flops) *alg_flops = c->prof.flops[kclass];
+  c->prof.bytes[kclass] = c->prof.flops[kclass] = 0.0;
+  return GSG_OK;
+}
 
 // ------------------------------------------------------------------------------ subgraph
 GSG_API int gsg_subgraph_upload(gsg_ctx_t c, int32_t n, int64_t nnz, const int64_t* h_indptr, const int32_t* h_indices,
@@ -230,6 +266,45 @@ GSG_API int gsg_subgraph_upload(gsg_ctx_t c, int32_t n, int64_t nnz, const int64
     e = cudaMemcpyAsync(sg->values, h_values, sizeof(float) * nnz, cudaMemcpyHostToDevice, c->stream);
   if (e != cudaSuccess) { gsg_subgraph_free(sg); return cuda_fail(e, "cudaMemcpyAsync(upload)"); }
   *out = sg;
+  return GSG_OK;
+}
+
+GSG_API int gsg_subgraph_assign(gsg_ctx_t c, gsg_subgraph_t sg, int32_t n, int64_t nnz, const int64_t* h_indptr,
+                                const int32_t* h_indices, const float* h_values, int validate) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
+  GSG_CHECK(n >= 0 && nnz >= 0, GSG_EINVAL, "negative n (%d) or nnz (%lld)", n, (long long)nnz);
+  GSG_CHECK(h_indptr && (nnz == 0 || h_indices), GSG_EINVAL, "NULL indptr/indices");
+  GSG_CHECK(nnz + (int64_t)n < (int64_t)INT32_MAX, GSG_EUNSUPPORTED, "nnz + n exceeds int32 indexing");
+  if (validate) {
+    if (int rc = validate_csr(n, nnz, h_indptr, h_indices)) return rc;
+  } else {
+    GSG_CHECK(h_indptr[n] == nnz, GSG_EGRAPH, "indptr[n] = %lld != nnz = %lld", (long long)h_indptr[n], (long long)nnz);
+  }
+  DeviceGuard dg(c->device);
+  if (n > sg->cap_n) {
+    cudaFree(sg->indptr); cudaFree(sg->rowptr); cudaFree(sg->perm);
+    sg->indptr = nullptr; sg->rowptr = sg->perm = nullptr;
+    GSG_CUDA(cudaMalloc((void**)&sg->indptr, sizeof(int64_t) * (n + 1)));
+    GSG_CUDA(cudaMalloc((void**)&sg->rowptr, sizeof(int32_t) * (n + 1)));
+    GSG_CUDA(cudaMalloc((void**)&sg->perm, sizeof(int32_t) * (n > 0 ? n : 1)));
+    sg->cap_n = n;
+  }
+  if (nnz > sg->cap_nnz) {
+    cudaFree(sg->indices); cudaFree(sg->values);
+    sg->indices = nullptr; sg->values = nullptr;
+    GSG_CUDA(cudaMalloc((void**)&sg->indices, sizeof(int32_t) * nnz));
+    sg->cap_nnz = nnz;
+  }
+  if (h_values && !sg->values) GSG_CUDA(cudaMalloc((void**)&sg->values, sizeof(float) * (sg->cap_nnz > 0 ? sg->cap_nnz : 1)));
+  sg->n = n;
+  sg->nnz = nnz;
+  sg->norm_mode = -1;
+  sg->has_values = h_values != nullptr;
+  GSG_CUDA(cudaMemcpyAsync(sg->indptr, h_indptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, c->stream));
+  if (nnz) GSG_CUDA(cudaMemcpyAsync(sg->indices, h_indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c->stream));
+  if (h_values && nnz)
+    GSG_CUDA(cudaMemcpyAsync(sg->values, h_values, sizeof(float) * nnz, cudaMemcpyHostToDevice, c->stream));
   return GSG_OK;
 }
 

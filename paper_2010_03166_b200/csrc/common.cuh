@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "gsg.h"
 
@@ -47,7 +48,25 @@ struct DevBuf {
 
 }  // namespace gsg
 
+namespace gsg {
+// Per-class CUDA-event profiler (gsg_ctx_profile).
+struct Profiler {
+  bool on = false;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> free_ev;
+  double bytes[GSG_K_CLASSES] = {}, flops[GSG_K_CLASSES] = {};
+  cudaEvent_t get() {
+    if (!free_ev.empty()) { cudaEvent_t e = free_ev.back(); free_ev.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+}  // namespace gsg
+
 struct gsg_ctx {
+  gsg::Profiler prof;
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -69,6 +88,9 @@ struct gsg_subgraph {
   int64_t nnz_hat = 0;      // entries of Â (after normalization)
   int norm_mode = -1;
   int32_t host_max_deg = -1;
+  int32_t cap_n = 0;        // allocated capacity (gsg_subgraph_assign reuses arrays)
+  int64_t cap_nnz = 0;
+  bool has_values = false;
   // raw structure (device)
   int64_t* indptr = nullptr;    // [n+1]
   int32_t* indices = nullptr;   // [nnz]
@@ -85,6 +107,26 @@ struct gsg_subgraph {
 
 namespace gsg {
 inline void count_launch(gsg_ctx* c, int k = 1) { c->launches += k; }
+
+// Brackets the kernels of one API-level launch with events when profiling is on.
+struct ProfScope {
+  gsg_ctx* c;
+  int cls;
+  cudaEvent_t a = nullptr;
+  ProfScope(gsg_ctx* c_, int cls_, double bytes, double flops) : c(c_), cls(cls_) {
+    if (!c->prof.on) return;
+    c->prof.bytes[cls] += bytes;
+    c->prof.flops[cls] += flops;
+    a = c->prof.get();
+    cudaEventRecord(a, c->stream);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEvent_t b = c->prof.get();
+    cudaEventRecord(b, c->stream);
+    c->prof.recs.push_back({cls, a, b});
+  }
+};
 
 // launch wrappers implemented in the .cu files
 int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode);

@@ -102,6 +102,7 @@ int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh,
   GSG_CHECK(lddh % 4 == 0 && ldh % 4 == 0 && lddz % 4 == 0 && (!dZlp || lddzlp % 8 == 0), GSG_EINVAL,
             "mask: strides must be multiples of 4 (bf16: 8)");
   if (rows == 0 || cols == 0) return GSG_OK;
+  ProfScope ps(ctx, GSG_K_OTHER, 12.0 * rows * cols, 0.0);
   const int cols4 = (cols + 3) / 4;
   const int64_t total = (int64_t)rows * cols4;
   int grid = (int)((total + 255) / 256);
@@ -118,6 +119,7 @@ int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64
   int rc = ctx->ws_loss.reserve(sizeof(float) * kHeadBlocks);
   if (rc) return rc;
   float* part = (float*)ctx->ws_loss.ptr;
+  ProfScope ps(ctx, GSG_K_OTHER, 9.0 * n * C, 0.0);
   k_head<<<kHeadBlocks, kHeadThreads, 0, ctx->stream>>>(n, C, kind, S, lds,
                                                         kind == GSG_HEAD_SOFTMAX ? (const int32_t*)labels : nullptr,
                                                         kind == GSG_HEAD_SIGMOID ? (const uint8_t*)labels : nullptr,

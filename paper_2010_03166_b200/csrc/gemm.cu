@@ -490,6 +490,8 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
             GSG_EINVAL, "EPI_MASK needs aux with ldaux >= N, ldaux %% 4 == 0, 16B alignment");
   if (M == 0 || N == 0) return GSG_OK;
   const bool bf16 = precision == GSG_PREC_BF16;
+  ProfScope ps(ctx, GSG_K_GEMM,
+               (double)(bf16 ? 2 : 4) * ((double)M * K + (double)K * N) + 4.0 * M * N, 2.0 * M * N * K);
   const int elem = bf16 ? 2 : 4;
   GemmArgs g{};
   g.M = M; g.N = N; g.K = K;
@@ -565,6 +567,7 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
 int to_bf16_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t lds, void* dst, int64_t ldd) {
   GSG_CHECK(rows >= 0 && cols >= 0 && lds >= cols && ldd >= cols, GSG_EINVAL, "bad to_bf16 shape");
   if (rows == 0 || cols == 0) return GSG_OK;
+  ProfScope ps(ctx, GSG_K_OTHER, 6.0 * rows * cols, 0.0);
   int64_t total = (int64_t)rows * cols;
   int grid = (int)((total + 255) / 256);
   if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;

@@ -120,7 +120,7 @@ __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t
 
 int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   GSG_CHECK(mode >= GSG_NORM_ROW_SELF && mode <= GSG_NORM_VALUES, GSG_EINVAL, "bad norm_mode %d", mode);
-  GSG_CHECK(mode != GSG_NORM_VALUES || sg->values, GSG_EINVAL, "GSG_NORM_VALUES needs uploaded edge values");
+  GSG_CHECK(mode != GSG_NORM_VALUES || sg->has_values, GSG_EINVAL, "GSG_NORM_VALUES needs uploaded edge values");
   const int self = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_SYM_SELF);
   const int64_t nh = sg->nnz + (self ? sg->n : 0);
   GSG_CHECK(nh < (int64_t)INT32_MAX, GSG_EUNSUPPORTED, "nnz_hat %lld exceeds int32", (long long)nh);
@@ -137,6 +137,7 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   }
   sg->nnz_hat = nh;
   sg->norm_mode = mode;
+  ProfScope ps(ctx, GSG_K_NORM, 16.0 * nh + 24.0 * n, 0.0);
   GSG_CUDA(cudaMemsetAsync(sg->counters, 0, sizeof(int32_t) * (3 * kBins + 8), st));
   const int T = 256;
   int grid = (n + 1 + T - 1) / T;
@@ -146,7 +147,7 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   if (n > 0) {
     int wgrid = (int)(((int64_t)n * 32 + T - 1) / T);
     if (wgrid > ctx->num_sms * 16) wgrid = ctx->num_sms * 16;
-    k_fill<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->indices, sg->values, mode, sg->rowptr, sg->col, sg->val);
+    k_fill<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode, sg->rowptr, sg->col, sg->val);
     k_transpose_vals<<<wgrid, T, 0, st>>>(n, sg->rowptr, sg->col, sg->val, sg->valT, sg->counters + 3 * kBins + 4);
     k_bin_offsets<<<1, 32, 0, st>>>(sg->counters);
     k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm);

@@ -225,6 +225,9 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
             "mask needs ldm >= f, ldm %% 4 == 0 and 16-byte alignment");
   GSG_CHECK(X != Y, GSG_EINVAL, "Y must not alias X");
   if (sg->n == 0) return GSG_OK;
+  // algorithmic (effective gather) bytes, SURVEY §8(d)
+  const double nh = (double)sg->nnz_hat, nn = (double)sg->n;
+  ProfScope ps(ctx, GSG_K_SPMM, 4.0 * nh * f + 8.0 * nh + 4.0 * (nn + 1) + 4.0 * nn * f, 2.0 * nh * f);
   SpmmArgs a;
   a.n = sg->n;
   a.f4 = (f + 3) / 4;

@@ -1,0 +1,111 @@
+"""One data-parallel training step of an L-layer GCN on a sampled subgraph, composed only of
+C-ABI calls (every row of SURVEY §8(a)):
+
+  a1  gsg_subgraph_normalize                      Â, Âᵀ values, degree bins
+  a2  gsg_layer_forward: P = Â X                  (fp32 SpMM)
+  a3                     H = ReLU(P W)            (tcgen05 GEMM, fused ReLU)
+  a8  gsg_head           S, CE loss, dS, dW_mlp, dH_L = (dS W_mlpᵀ) ⊙ 1[H_L > 0]
+  a4-a7 gsg_layer_backward (top down):  dW = Pᵀ dZ ; T = dZ Wᵀ ; dX = Âᵀ T ⊙ 1[H_below > 0]
+  a9  gsg_allreduce_grads                         NCCL mean of all dW (one flat buffer)
+
+This mirrors Alg. 1 lines 3-13 minus the weight update, for the GCN model
+of Eq. 5 with the backward of P:719. Buffers are allocated once for the largest
+subgraph; the step itself allocates nothing (CUDA-graph friendly).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import (GSG_DH_PREMASKED, GSG_HEAD_SIGMOID, GSG_HEAD_SOFTMAX, GSG_NORM_ROW_SELF, GSG_PREC_BF16,
+               GSG_PREC_TF32, Context, Subgraph)
+
+
+def ld_for(f: int, align: int = 8) -> int:
+    return (f + align - 1) // align * align
+
+
+def padded(rows: int, f: int, dtype=torch.float32, align: int = 8, device="cuda"):
+    """Row-major [rows x f] view of a [rows x ld] buffer (ld multiple of 8 elements)."""
+    return torch.zeros((rows, ld_for(f, align)), dtype=dtype, device=device)[:, :f]
+
+
+class GCNStep:
+    def __init__(self, ctx: Context, dims: list, n_max: int, head: str = "none", classes: int = 0,
+                 precision: str = "tf32", device: int = 0, weights=None, w_mlp=None):
+        self.ctx, self.dims, self.n_max = ctx, list(dims), n_max
+        self.L = len(dims) - 1
+        self.head = head
+        self.C = classes
+        self.prec = GSG_PREC_BF16 if precision == "bf16" else GSG_PREC_TF32
+        dev = torch.device("cuda", device)
+        bf = self.prec == GSG_PREC_BF16
+        self.W = [padded(dims[l], dims[l + 1], device=dev) for l in range(self.L)]
+        if weights is not None:
+            for w, src in zip(self.W, weights):
+                w.copy_(torch.as_tensor(src))
+        self.P = [padded(n_max, dims[l], device=dev) for l in range(self.L)]
+        self.H = [padded(n_max, dims[l + 1], device=dev) for l in range(self.L)]
+        self.dX = [padded(n_max, dims[l], device=dev) for l in range(self.L)]
+        self.Plp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
+        self.dXlp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
+        # all weight gradients in one flat buffer -> one allreduce (a9)
+        # (rows padded to 16-byte strides; the padding is reduced along harmlessly)
+        shapes = [(dims[l], dims[l + 1]) for l in range(self.L)]
+        if head != "none":
+            shapes.append((dims[-1], classes))
+        sizes = [r * ld_for(c, 4) for r, c in shapes]
+        self.grad_flat = torch.zeros(sum(sizes), dtype=torch.float32, device=dev)
+        views, off = [], 0
+        for (r, c), s in zip(shapes, sizes):
+            views.append(self.grad_flat[off:off + s].view(r, ld_for(c, 4))[:, :c])
+            off += s
+        self.dW = views[:self.L]
+        if head != "none":
+            self.Wm = padded(dims[-1], classes, device=dev)
+            if w_mlp is not None:
+                self.Wm.copy_(torch.as_tensor(w_mlp))
+            self.dWm = views[self.L]
+            self.S = padded(n_max, classes, device=dev)
+            self.dS = torch.zeros((n_max, self.S.stride(0)), device=dev)[:, :classes]
+            self.dHL = padded(n_max, dims[-1], device=dev)
+            self.dHLlp = padded(n_max, dims[-1], torch.bfloat16, device=dev) if bf else None
+        self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
+
+    def forward_backward(self, sg: Subgraph, X, labels=None, dH_top=None, comm=None, normalize: bool = True):
+        ctx, d, n = self.ctx, self.dims, sg.n
+        if normalize:
+            sg.normalize(GSG_NORM_ROW_SELF)
+        h = X
+        for l in range(self.L):
+            ctx.layer_forward(sg, h, self.W[l], self.P[l][:n], self.H[l][:n], d[l], d[l + 1], precision=self.prec,
+                              Plp=None if self.Plp[l] is None else self.Plp[l][:n])
+            h = self.H[l][:n]
+        if self.head != "none":
+            kind = GSG_HEAD_SOFTMAX if self.head == "softmax" else GSG_HEAD_SIGMOID
+            ctx.head(h, self.Wm, labels, self.S[:n], self.dS[:n], self.dWm, self.dHL[:n], n, d[-1], self.C, kind,
+                     self.loss, dHlp=None if self.dHLlp is None else self.dHLlp[:n])
+            dH, dHlp, flags = self.dHL[:n], (None if self.dHLlp is None else self.dHLlp[:n]), GSG_DH_PREMASKED
+        else:
+            dH, dHlp, flags = dH_top, None, 0
+        for l in range(self.L - 1, -1, -1):
+            Hb = self.H[l - 1][:n] if l > 0 else None
+            ctx.layer_backward(sg, self.P[l][:n], self.H[l][:n], dH, self.W[l], self.dW[l], self.dX[l][:n],
+                               d[l], d[l + 1], precision=self.prec,
+                               Plp=None if self.Plp[l] is None else self.Plp[l][:n], dHlp=dHlp,
+                               dXlp=None if self.dXlp[l] is None else self.dXlp[l][:n], H_below=Hb, flags=flags)
+            dH = self.dX[l][:n]
+            dHlp = None if self.dXlp[l] is None else self.dXlp[l][:n]
+            flags = GSG_DH_PREMASKED  # the transposed aggregation already applied layer l-1's ReLU' gate
+        if comm is not None:
+            ctx.allreduce_grads(comm, [self.grad_flat], average=True)
+        return self.loss
+
+    def work_edge_features(self, nnz_hat: int) -> int:
+        """2 * nnz' * f_in edge-features per layer (a2 + a7), summed over layers."""
+        return sum(2 * nnz_hat * self.dims[l] for l in range(self.L))
+
+    def gemm_flops(self, n: int) -> int:
+        f = 6 * sum(n * self.dims[l] * self.dims[l + 1] for l in range(self.L))
+        if self.head != "none":
+            f += 6 * n * self.dims[-1] * self.C
+        return f
