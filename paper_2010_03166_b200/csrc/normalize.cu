@@ -31,9 +31,14 @@ __global__ void k_rowptr(int n, const int64_t* __restrict__ indptr, int self, in
 
 // One warp per row: copy the neighbor list inserting the self loop at its sorted position and
 // compute the values of the requested normalization in fp64 (rounded once to fp32).
+//
+// For the degree-based modes the transposed value is a closed form of the column's degree
+// (Âᵀ_ij = Â_ji: 1/(d_j+1) row-self, 1/d_j row, val itself for the symmetric mode), written
+// here in the same fp64 -> fp32 rounding as Â_ji, so valT is bit-for-bit the permutation of
+// val that Alg. 4 produces. GSG_NORM_VALUES needs the search (k_transpose_vals).
 __global__ void k_fill(int n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                        const float* __restrict__ values, int mode, const int32_t* __restrict__ rowptr,
-                       int32_t* __restrict__ col, float* __restrict__ val) {
+                       int32_t* __restrict__ col, float* __restrict__ val, float* __restrict__ valT) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int self = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_SYM_SELF);
@@ -50,19 +55,27 @@ __global__ void k_fill(int n, const int64_t* __restrict__ indptr, const int32_t*
       const unsigned lt = __ballot_sync(0xffffffffu, ok && j < i);
       if (ok) {
         const int pos = (int)(k - b) + (self && j > i ? 1 : 0);
-        double a;
-        if (mode == GSG_NORM_ROW_SELF) a = 1.0 / (di + 1.0);
-        else if (mode == GSG_NORM_SYM_SELF) a = 1.0 / sqrt((di + 1.0) * ((double)(indptr[j + 1] - indptr[j]) + 1.0));
-        else if (mode == GSG_NORM_ROW) a = 1.0 / di;
-        else a = (double)values[k];
+        double a, at = 0.0;
+        if (mode == GSG_NORM_ROW_SELF) {
+          a = 1.0 / (di + 1.0);
+          at = 1.0 / ((double)(indptr[j + 1] - indptr[j]) + 1.0);
+        } else if (mode == GSG_NORM_SYM_SELF) {
+          a = at = 1.0 / sqrt((di + 1.0) * ((double)(indptr[j + 1] - indptr[j]) + 1.0));
+        } else if (mode == GSG_NORM_ROW) {
+          a = 1.0 / di;
+          at = 1.0 / (double)(indptr[j + 1] - indptr[j]);
+        } else {
+          a = (double)values[k];
+        }
         col[o + pos] = j;
         val[o + pos] = (float)a;
+        if (mode != GSG_NORM_VALUES) valT[o + pos] = (float)at;
       }
       below += __popc(lt);
     }
     if (self && lane == 0) {
       col[o + below] = i;
-      val[o + below] = (float)(1.0 / (di + 1.0));
+      val[o + below] = valT[o + below] = (float)(1.0 / (di + 1.0));
     }
   }
 }
@@ -147,11 +160,15 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   if (n > 0) {
     int wgrid = (int)(((int64_t)n * 32 + T - 1) / T);
     if (wgrid > ctx->num_sms * 16) wgrid = ctx->num_sms * 16;
-    k_fill<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode, sg->rowptr, sg->col, sg->val);
-    k_transpose_vals<<<wgrid, T, 0, st>>>(n, sg->rowptr, sg->col, sg->val, sg->valT, sg->counters + 3 * kBins + 4);
+    k_fill<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode, sg->rowptr,
+                                sg->col, sg->val, sg->valT);
+    if (mode == GSG_NORM_VALUES) {
+      k_transpose_vals<<<wgrid, T, 0, st>>>(n, sg->rowptr, sg->col, sg->val, sg->valT, sg->counters + 3 * kBins + 4);
+      count_launch(ctx);
+    }
     k_bin_offsets<<<1, 32, 0, st>>>(sg->counters);
     k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm);
-    count_launch(ctx, 5);
+    count_launch(ctx, 4);
   } else {
     count_launch(ctx, 1);
   }

@@ -2,13 +2,17 @@
 //
 // The product is Alg. 6's feature propagation re-designed for sm_100a:
 //   * The paper splits the feature columns into Q_f slabs, one per core, so each core's slab
-//     fits its private cache (Theorem 2). On B200 every SM should instead work on
-//     the SAME column slab at a time so the slab is shared through the 126 MB L2: tasks are
+//     fits its private cache (Theorem 2). On B200 every SM instead works on the
+//     SAME column slab at a time so the slab is shared through the 126 MB L2: tasks are
 //     ordered chunk-major (all rows of column chunk 0, then chunk 1, ...), so the concurrently
-//     running warps touch one n x 128-column slab (10 MB at n = 20,000).
-//   * One lane owns one float4 column group; a warp task is one (row, <=128-column chunk)
-//     pair; neighbor (idx, val) pairs are loaded 32 at a time and broadcast with __shfl_sync;
-//     8 independent 16-byte row gathers are in flight per lane.
+//     running warps touch one n x 256-column slab (20 MB at n = 20,000).
+//   * A warp task is one (row, <= 256-column chunk) pair; lane l owns float4 columns l and
+//     l + 32 of the chunk (V = 2), so every neighbor costs one 32-bit offset broadcast and two
+//     coalesced 512-byte row gathers. Neighbor (offset, value) pairs are staged 32 at a time in
+//     shared memory and read back as 128-bit broadcasts (two pairs per LDS.128); 8 neighbors'
+//     gathers (16 x 16 B per lane) are in flight per iteration; accumulation uses packed
+//     fp32x2 FMAs (FFMA2). The kernel is bound by L2->SM gather throughput (X is L2-resident),
+//     so instructions per gathered byte are what the design minimizes.
 //   * Degree bins (built by normalize): rows are visited in descending degree order, and
 //     "heavy" rows (deg' >= 256) are split across the 8 warps of a CTA whose partial sums are
 //     reduced through shared memory in a fixed warp order.
@@ -29,7 +33,8 @@ struct SpmmArgs {
   const int32_t* __restrict__ col;
   const float* __restrict__ val;
   const float4* __restrict__ X;
-  int64_t ldx4;
+  uint32_t ldx4;             // row stride of X in float4
+  uint32_t ldx16;            // row stride of X in bytes (n * ldx * 4 < 2^32 checked on the host)
   float4* __restrict__ Y;
   int64_t ldy4;
   uint2* __restrict__ Ylp;   // 4 bf16 per uint2
@@ -42,49 +47,86 @@ struct SpmmArgs {
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
+constexpr int V = 2;   // float4 per lane per neighbor (full-warp path)
+constexpr int U = 8;   // neighbors per unrolled iteration
 
-__device__ __forceinline__ void fma4(float a, const float4& v, float4& acc) {
-  acc.x = fmaf(a, v.x, acc.x);
-  acc.y = fmaf(a, v.y, acc.y);
-  acc.z = fmaf(a, v.z, acc.z);
-  acc.w = fmaf(a, v.w, acc.w);
+// acc += a * x on packed fp32 pairs (FFMA2, round-to-nearest per element: identical to two FFMAs)
+__device__ __forceinline__ void fma2(float2& acc, float a, float2 x) {
+  unsigned long long r;
+  const unsigned long long aa = ((unsigned long long)__float_as_uint(a) << 32) | __float_as_uint(a);
+  const unsigned long long xx = ((unsigned long long)__float_as_uint(x.y) << 32) | __float_as_uint(x.x);
+  const unsigned long long cc = ((unsigned long long)__float_as_uint(acc.y) << 32) | __float_as_uint(acc.x);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(aa), "l"(xx), "l"(cc));
+  acc.x = __uint_as_float((uint32_t)r);
+  acc.y = __uint_as_float((uint32_t)(r >> 32));
 }
 
-__device__ __forceinline__ float4 ldx(const float4* p) { return __ldg(p); }
+struct Acc {
+  float2 v[2 * V];
+};
 
-// Full-warp accumulation of sum_{k in [b, e)} val[k] * X[col[k], c4] (c4 = this lane's float4).
-__device__ __forceinline__ float4 warp_row_sum(const SpmmArgs& a, int b, int e, int c4, bool act, int lane) {
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4* Xc = a.X + c4;
+__device__ __forceinline__ void acc_fma(Acc& A, float w, const float4 (&x)[V]) {
+#pragma unroll
+  for (int q = 0; q < V; q++) {
+    fma2(A.v[2 * q], w, make_float2(x[q].x, x[q].y));
+    fma2(A.v[2 * q + 1], w, make_float2(x[q].z, x[q].w));
+  }
+}
+
+__device__ __forceinline__ const float4* row_ptr(const float4* X, uint32_t byte_off) {
+  return reinterpret_cast<const float4*>(reinterpret_cast<const char*>(X) + byte_off);
+}
+
+// Full-warp accumulation over neighbors [b, e) of this lane's float4 columns. Lanes whose
+// column falls outside the chunk read the chunk's last column instead (same sectors as an
+// active lane: no extra traffic, no predication); their sums are never stored.
+// FULL: every lane's columns are inside the chunk, so the second gather is the first + 512 B
+// (an immediate offset): per neighbor one 64-bit address add, two LDG.128, four FFMA2.
+template <bool FULL>
+__device__ __forceinline__ void warp_row_sum(const SpmmArgs& a, int2* __restrict__ st, int b, int e,
+                                             uint32_t lo0, uint32_t lo1, int lane, Acc& A) {
+  const float4* X = a.X;
+  const float4* X0 = row_ptr(X, lo0);
+#pragma unroll
+  for (int q = 0; q < 2 * V; q++) A.v[q] = make_float2(0.f, 0.f);
   for (int k0 = b; k0 < e; k0 += 32) {
     const int k = k0 + lane;
+    if (k < e) st[lane] = make_int2((int)((uint32_t)__ldg(a.col + k) * a.ldx16), __float_as_int(__ldg(a.val + k)));
+    __syncwarp();
     const int cnt = min(32, e - k0);
-    const int cj = k < e ? __ldg(a.col + k) : 0;
-    const float aj = k < e ? __ldg(a.val + k) : 0.f;
     int j = 0;
-    for (; j + 8 <= cnt; j += 8) {
-      int c[8];
-      float w[8];
-      float4 v[8];
+    for (; j + U <= cnt; j += U) {
+      int4 p[U / 2];
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
-        c[u] = __shfl_sync(0xffffffffu, cj, j + u);
-        w[u] = __shfl_sync(0xffffffffu, aj, j + u);
+      for (int q = 0; q < U / 2; q++) p[q] = reinterpret_cast<const int4*>(st)[(j >> 1) + q];
+      float4 x[U][V];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const uint32_t off = (u & 1) ? (uint32_t)p[u >> 1].z : (uint32_t)p[u >> 1].x;
+        if (FULL) {
+          const float4* r = row_ptr(X0, off);
+          x[u][0] = __ldg(r);
+          if (V == 2) x[u][1] = __ldg(r + 32);
+        } else {
+          x[u][0] = __ldg(row_ptr(X, off + lo0));
+          if (V == 2) x[u][1] = __ldg(row_ptr(X, off + lo1));
+        }
       }
-      if (act) {
 #pragma unroll
-        for (int u = 0; u < 8; u++) v[u] = ldx(Xc + (int64_t)c[u] * a.ldx4);
-#pragma unroll
-        for (int u = 0; u < 8; u++) fma4(w[u], v[u], acc);
+      for (int u = 0; u < U; u++) {
+        const float w = __int_as_float((u & 1) ? p[u >> 1].w : p[u >> 1].y);
+        acc_fma(A, w, x[u]);
       }
     }
     for (; j < cnt; j++) {
-      const int c = __shfl_sync(0xffffffffu, cj, j);
-      const float w = __shfl_sync(0xffffffffu, aj, j);
-      if (act) fma4(w, ldx(Xc + (int64_t)c * a.ldx4), acc);
+      const int2 p = st[j];
+      float4 x[V];
+      x[0] = __ldg(row_ptr(X, (uint32_t)p.x + lo0));
+      if (V == 2) x[1] = __ldg(row_ptr(X, (uint32_t)p.x + lo1));
+      acc_fma(A, __int_as_float(p.y), x);
     }
+    __syncwarp();
   }
-  return acc;
 }
 
 // Sub-warp (group of G lanes, one row) accumulation; no shuffles (groups diverge).
@@ -93,22 +135,33 @@ __device__ __forceinline__ float4 group_row_sum(const SpmmArgs& a, int b, int e,
   const float4* Xc = a.X + c4;
   int k = b;
   for (; k + 4 <= e; k += 4) {
-    int c[4];
+    uint32_t c[4];
     float w[4];
     float4 v[4];
 #pragma unroll
-    for (int u = 0; u < 4; u++) { c[u] = __ldg(a.col + k + u); w[u] = __ldg(a.val + k + u); }
+    for (int u = 0; u < 4; u++) { c[u] = (uint32_t)__ldg(a.col + k + u) * a.ldx4; w[u] = __ldg(a.val + k + u); }
     if (act) {
 #pragma unroll
-      for (int u = 0; u < 4; u++) v[u] = ldx(Xc + (int64_t)c[u] * a.ldx4);
+      for (int u = 0; u < 4; u++) v[u] = __ldg(Xc + c[u]);
 #pragma unroll
-      for (int u = 0; u < 4; u++) fma4(w[u], v[u], acc);
+      for (int u = 0; u < 4; u++) {
+        acc.x = fmaf(w[u], v[u].x, acc.x);
+        acc.y = fmaf(w[u], v[u].y, acc.y);
+        acc.z = fmaf(w[u], v[u].z, acc.z);
+        acc.w = fmaf(w[u], v[u].w, acc.w);
+      }
     }
   }
   for (; k < e; k++) {
-    const int c = __ldg(a.col + k);
+    const uint32_t c = (uint32_t)__ldg(a.col + k) * a.ldx4;
     const float w = __ldg(a.val + k);
-    if (act) fma4(w, ldx(Xc + (int64_t)c * a.ldx4), acc);
+    if (act) {
+      const float4 v = __ldg(Xc + c);
+      acc.x = fmaf(w, v.x, acc.x);
+      acc.y = fmaf(w, v.y, acc.y);
+      acc.z = fmaf(w, v.z, acc.z);
+      acc.w = fmaf(w, v.w, acc.w);
+    }
   }
   return acc;
 }
@@ -132,13 +185,19 @@ __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int c4, fl
   }
 }
 
-template <int G>
-__global__ void __launch_bounds__(kThreads) k_spmm(SpmmArgs a) {
-  __shared__ float4 part[kWarps][32];
+__device__ __forceinline__ float4 acc_part(const Acc& A, int q) {
+  return make_float4(A.v[2 * q].x, A.v[2 * q].y, A.v[2 * q + 1].x, A.v[2 * q + 1].y);
+}
+
+// Full-warp kernel (f > 64): chunk = up to 64 float4 (256 columns), lane owns c4 and c4 + 32.
+__global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
+  __shared__ __align__(16) int2 stage[kWarps][32];
+  __shared__ float4 part[kWarps][32 * V];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int n_heavy = *a.n_heavy_ptr;
   const int n_light = a.n - n_heavy;
+  int2* st = stage[warp];
 
   // ---- phase 1: heavy rows, one CTA per (row, chunk), neighbors split across 8 warps ----
   const int64_t H = (int64_t)n_heavy * a.nchunks;
@@ -149,8 +208,67 @@ __global__ void __launch_bounds__(kThreads) k_spmm(SpmmArgs a) {
     const int seg = (e - b + kWarps - 1) / kWarps;
     const int w0 = min(e, b + warp * seg), w1 = min(e, w0 + seg);
     const int c4 = chunk * a.cw + lane;
-    const bool act = lane < a.cw && c4 < a.f4;
-    part[warp][lane] = warp_row_sum(a, w0, w1, c4, act, lane);
+    const int lim = min(a.f4, (chunk + 1) * a.cw);
+    const bool act0 = c4 < lim, act1 = c4 + 32 < lim;
+    Acc A;
+    if (a.cw == 32 * V && lim == (chunk + 1) * a.cw)
+      warp_row_sum<true>(a, st, w0, w1, 16u * c4, 16u * (c4 + 32), lane, A);
+    else
+      warp_row_sum<false>(a, st, w0, w1, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
+    part[warp][lane] = acc_part(A, 0);
+    part[warp][lane + 32] = acc_part(A, 1);
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < V; q++) {
+        float4 s = part[0][lane + 32 * q];
+#pragma unroll
+        for (int w = 1; w < kWarps; w++) {
+          const float4 p = part[w][lane + 32 * q];
+          s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
+        }
+        if (q == 0 ? act0 : act1) store_row(a, row, c4 + 32 * q, s);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- phase 2: light rows, one warp per (row, chunk) ----
+  const int64_t L = (int64_t)n_light * a.nchunks;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t GW = (int64_t)gridDim.x * kWarps;
+  for (int64_t t = gw; t < L; t += GW) {
+    const int chunk = (int)(t / n_light);
+    const int row = a.perm[n_heavy + (int)(t % n_light)];
+    const int c4 = chunk * a.cw + lane;
+    const int lim = min(a.f4, (chunk + 1) * a.cw);
+    const bool act0 = c4 < lim, act1 = c4 + 32 < lim;
+    Acc A;
+    const int b = a.rowptr[row], e = a.rowptr[row + 1];
+    if (a.cw == 32 * V && lim == (chunk + 1) * a.cw)
+      warp_row_sum<true>(a, st, b, e, 16u * c4, 16u * (c4 + 32), lane, A);
+    else
+      warp_row_sum<false>(a, st, b, e, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
+    if (act0) store_row(a, row, c4, acc_part(A, 0));
+    if (act1) store_row(a, row, c4 + 32, acc_part(A, 1));
+  }
+}
+
+// Sub-warp kernel (f <= 64): groups of G lanes, one row per group; heavy rows CTA-split.
+template <int G>
+__global__ void __launch_bounds__(kThreads) k_spmm_narrow(SpmmArgs a) {
+  __shared__ float4 part[kWarps][32];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int n_heavy = *a.n_heavy_ptr;
+  const int n_light = a.n - n_heavy;
+  for (int64_t t = blockIdx.x; t < n_heavy; t += gridDim.x) {
+    const int row = a.perm[t];
+    const int b = a.rowptr[row], e = a.rowptr[row + 1];
+    const int seg = (e - b + kWarps - 1) / kWarps;
+    const int w0 = min(e, b + warp * seg), w1 = min(e, w0 + seg);
+    const bool act = lane < a.f4;
+    part[warp][lane] = group_row_sum(a, w0, w1, lane, act);
     __syncthreads();
     if (warp == 0) {
       float4 s = part[0][lane];
@@ -159,51 +277,34 @@ __global__ void __launch_bounds__(kThreads) k_spmm(SpmmArgs a) {
         const float4 p = part[w][lane];
         s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
       }
-      if (act) store_row(a, row, c4, s);
+      if (act) store_row(a, row, lane, s);
     }
     __syncthreads();
   }
-
-  // ---- phase 2: light rows ----
-  if (G == 32) {
-    const int64_t L = (int64_t)n_light * a.nchunks;
-    const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
-    const int64_t GW = (int64_t)gridDim.x * kWarps;
-    for (int64_t t = gw; t < L; t += GW) {
-      const int chunk = (int)(t / n_light);
-      const int row = a.perm[n_heavy + (int)(t % n_light)];
-      const int c4 = chunk * a.cw + lane;
-      const bool act = lane < a.cw && c4 < a.f4;
-      const float4 acc = warp_row_sum(a, a.rowptr[row], a.rowptr[row + 1], c4, act, lane);
-      if (act) store_row(a, row, c4, acc);
-    }
-  } else {
-    constexpr int PER = 32 / G;
-    const int g = lane / G, gl = lane % G;
-    const int64_t gid = ((int64_t)blockIdx.x * kWarps + warp) * PER + g;
-    const int64_t GN = (int64_t)gridDim.x * kWarps * PER;
-    const bool act = gl < a.f4;
-    for (int64_t t = gid; t < n_light; t += GN) {
-      const int row = a.perm[n_heavy + (int)t];
-      const float4 acc = group_row_sum(a, a.rowptr[row], a.rowptr[row + 1], gl, act);
-      if (act) store_row(a, row, gl, acc);
-    }
+  constexpr int PER = 32 / G;
+  const int g = lane / G, gl = lane % G;
+  const int64_t gid = ((int64_t)blockIdx.x * kWarps + warp) * PER + g;
+  const int64_t GN = (int64_t)gridDim.x * kWarps * PER;
+  const bool act = gl < a.f4;
+  for (int64_t t = gid; t < n_light; t += GN) {
+    const int row = a.perm[n_heavy + (int)t];
+    const float4 acc = group_row_sum(a, a.rowptr[row], a.rowptr[row + 1], gl, act);
+    if (act) store_row(a, row, gl, acc);
   }
 }
 
-template <int G>
-int launch_g(gsg_ctx* ctx, const SpmmArgs& a, int64_t tasks) {
-  static int occ = -1;
-  if (occ < 0) {
+template <typename K>
+int launch_k(gsg_ctx* ctx, K kern, int* occ_cache, const SpmmArgs& a, int64_t warp_tasks) {
+  if (*occ_cache < 0) {
     int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_spmm<G>, kThreads, 0) != cudaSuccess || o < 1) o = 1;
-    occ = o;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, 0) != cudaSuccess || o < 1) o = 1;
+    *occ_cache = o;
   }
-  int64_t want = (tasks + kWarps - 1) / kWarps;
-  int64_t grid = (int64_t)ctx->num_sms * occ;
+  int64_t want = (warp_tasks + kWarps - 1) / kWarps;
+  int64_t grid = (int64_t)ctx->num_sms * *occ_cache;
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
-  k_spmm<G><<<(int)grid, kThreads, 0, ctx->stream>>>(a);
+  kern<<<(int)grid, kThreads, 0, ctx->stream>>>(a);
   count_launch(ctx);
   GSG_CUDA(cudaGetLastError());
   return GSG_OK;
@@ -224,6 +325,8 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   GSG_CHECK(!mask || (ldm >= f && ldm % 4 == 0 && (uintptr_t)mask % 16 == 0), GSG_EINVAL,
             "mask needs ldm >= f, ldm %% 4 == 0 and 16-byte alignment");
   GSG_CHECK(X != Y, GSG_EINVAL, "Y must not alias X");
+  GSG_CHECK((int64_t)sg->n * ldx * 4 < ((int64_t)1 << 32), GSG_EUNSUPPORTED,
+            "X too large for 32-bit byte offsets (n * ldx * 4 >= 4 GiB)");
   if (sg->n == 0) return GSG_OK;
   // algorithmic (effective gather) bytes, SURVEY §8(d)
   const double nh = (double)sg->nnz_hat, nn = (double)sg->n;
@@ -235,7 +338,8 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   a.col = sg->col;
   a.val = transpose ? sg->valT : sg->val;
   a.X = reinterpret_cast<const float4*>(X);
-  a.ldx4 = ldx / 4;
+  a.ldx4 = (uint32_t)(ldx / 4);
+  a.ldx16 = (uint32_t)(ldx * 4);
   a.Y = reinterpret_cast<float4*>(Y);
   a.ldy4 = ldy / 4;
   a.Ylp = reinterpret_cast<uint2*>(Ylp);
@@ -244,16 +348,17 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   a.ldm4 = ldm / 4;
   a.perm = sg->perm;
   a.n_heavy_ptr = sg->counters + kBins;
+  static int occ_wide = -1, occ16 = -1, occ8 = -1, occ4 = -1;
   if (a.f4 > 16) {
-    a.nchunks = (a.f4 + 31) / 32;
+    a.nchunks = (a.f4 + 32 * V - 1) / (32 * V);
     a.cw = (a.f4 + a.nchunks - 1) / a.nchunks;
-    return launch_g<32>(ctx, a, (int64_t)sg->n * a.nchunks);
+    return launch_k(ctx, k_spmm_wide, &occ_wide, a, (int64_t)sg->n * a.nchunks);
   }
   a.nchunks = 1;
   a.cw = a.f4;
-  if (a.f4 > 8) return launch_g<16>(ctx, a, (int64_t)sg->n / 2 + 1);
-  if (a.f4 > 4) return launch_g<8>(ctx, a, (int64_t)sg->n / 4 + 1);
-  return launch_g<4>(ctx, a, (int64_t)sg->n / 8 + 1);
+  if (a.f4 > 8) return launch_k(ctx, k_spmm_narrow<16>, &occ16, a, (int64_t)sg->n / 2 + 1);
+  if (a.f4 > 4) return launch_k(ctx, k_spmm_narrow<8>, &occ8, a, (int64_t)sg->n / 4 + 1);
+  return launch_k(ctx, k_spmm_narrow<4>, &occ4, a, (int64_t)sg->n / 8 + 1);
 }
 
 }  // namespace gsg
