@@ -113,48 +113,55 @@ def dist_env():
 
 
 # ------------------------------------------------------------------------------ oracle leg
-def oracle_sample(cfg, csr, inputs, target_s: float, seed: int = 0):
-    """Time the fp64 oracle (oracle/, as it stands) on a bounded row sample of one step of
+class OracleSample:
+    """Times the fp64 oracle (oracle/, as it stands) on a bounded row sample of one step of
     this workload: for every layer the aggregation, transform, ReLU' gate, dW, T and the
     scatter-form transpose restricted to output/source rows [0, R) (plus the head on the same
-    rows), R calibrated so the sample takes about `target_s` seconds. Returns (edge-features
-    per second, details)."""
-    import oracle as orc
-    A = orc.normalize(csr.indptr, csr.indices, orc.NORM_ROW_SELF)
-    rng = np.random.default_rng(seed)
-    dims = cfg.dims
-    # stand-in layer inputs (values do not affect the oracle's run time)
-    hs = [np.ascontiguousarray(inputs.X, np.float64)] + [np.abs(rng.standard_normal((csr.n, f))) for f in dims[1:-1]]
-    Ws = [np.asarray(w, np.float64) for w in inputs.Ws]
-    dHs = [rng.standard_normal((csr.n, f)) for f in dims[1:]]
-    rowptr = A.indptr
+    rows). Stand-in layer inputs are random (values do not affect the oracle's run time)."""
 
-    def run(R):
+    def __init__(self, cfg, csr, inputs, seed: int = 0):
+        import oracle as orc
+        self.orc, self.cfg, self.csr, self.inputs = orc, cfg, csr, inputs
+        self.A = orc.normalize(csr.indptr, csr.indices, orc.NORM_ROW_SELF)
+        rng = np.random.default_rng(seed)
+        dims = cfg.dims
+        self.hs = [np.ascontiguousarray(inputs.X, np.float64)] + \
+            [np.abs(rng.standard_normal((csr.n, f))) for f in dims[1:-1]]
+        self.Ws = [np.asarray(w, np.float64) for w in inputs.Ws]
+        self.dHs = [rng.standard_normal((csr.n, f)) for f in dims[1:]]
+        self.rows = None
+
+    def run(self, R: int):
+        orc, cfg, dims, A = self.orc, self.cfg, self.cfg.dims, self.A
         work = 0
         t0 = time.perf_counter()
         for l in range(cfg.L):
-            P = orc.spmm(A, hs[l], 0, R)
-            Z = orc.gemm(P[:R], Ws[l])
-            dZ = orc.relu_mask(dHs[l][:R], Z)
+            P = orc.spmm(A, self.hs[l], 0, R)
+            Z = orc.gemm(P[:R], self.Ws[l])
+            dZ = orc.relu_mask(self.dHs[l][:R], Z)
             orc.gemm(P[:R], dZ, transA=True)
-            T = np.zeros((csr.n, dims[l]))
-            T[:R] = orc.gemm(dZ, Ws[l], transB=True)
+            T = np.zeros((self.csr.n, dims[l]))
+            T[:R] = orc.gemm(dZ, self.Ws[l], transB=True)
             orc.spmm_t(A, T, 0, R)
-            work += 2 * int(rowptr[R]) * dims[l]
+            work += 2 * int(A.indptr[R]) * dims[l]
         if cfg.head != "none":
-            S = orc.gemm(np.maximum(Z, 0), inputs.W_mlp)
-            lab = inputs.labels[:R]
-            _, _, dS = orc.head(S, lab, cfg.head)
-            orc.head_backward(np.maximum(Z, 0), dS, inputs.W_mlp)
+            S = orc.gemm(np.maximum(Z, 0), self.inputs.W_mlp)
+            _, _, dS = orc.head(S, self.inputs.labels[:R], cfg.head)
+            orc.head_backward(np.maximum(Z, 0), dS, self.inputs.W_mlp)
         return work, time.perf_counter() - t0
 
-    R = min(64, csr.n)
-    work, dt = run(R)
-    while dt < 0.2 * target_s and R < csr.n:
-        R = min(csr.n, max(R + 1, int(R * min(8.0, 0.8 * target_s / max(dt, 1e-3)))))
-        work, dt = run(R)
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return work / dt, {"rows": R, "seconds": dt, "work": work, "cores": cores}
+    def calibrate(self, target_s: float):
+        R = min(64, self.csr.n)
+        work, dt = self.run(R)
+        while dt < 0.2 * target_s and R < self.csr.n:
+            R = min(self.csr.n, max(R + 1, int(R * min(8.0, 0.8 * target_s / max(dt, 1e-3)))))
+            work, dt = self.run(R)
+        self.rows = R
+        return work, dt
+
+    @staticmethod
+    def cores():
+        return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
 
 def run_reference(args, cfg):
@@ -163,14 +170,16 @@ def run_reference(args, cfg):
         return 0
     g = wl.sample_subgraph(cfg, 0, 0)
     inp = wl.make_inputs(cfg, g.n, 0, 0)
-    per_step = max(1.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step = max(0.5, min(8.0, 120.0 / max(1, args.steps + args.warmup)))
     vals = []
-    info = None
+    osamp = OracleSample(cfg, g, inp)
+    osamp.calibrate(per_step)  # size the row sample once
     for i in range(args.warmup + args.steps):
-        v, info = oracle_sample(cfg, g, inp, per_step, seed=i)
+        work, dt = osamp.run(osamp.rows)
         if i >= args.warmup:
-            vals.append(v)
+            vals.append(work / dt)
     value = float(statistics.median(vals)) if vals else 0.0
+    info = {"rows": osamp.rows, "cores": osamp.cores()}
     sample = (f"rows [0,{info['rows']}) of rank 0's config-{cfg.cid} subgraph (n={g.n}, nnz'={g.nnz + g.n}): "
               f"all {cfg.L} layers' aggregation, transform, gate, dW, T, transposed scatter + head, fp64")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -206,6 +215,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2010_03166_b200 as gsg
+    from paper_2010_03166_b200 import dp
     from paper_2010_03166_b200.step import GCNStep
 
     rank, world, local = dist_env()
@@ -244,9 +254,8 @@ def main():
     stream.synchronize()
     comm = None
     if world > 1:
-        uid = [ctx.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = ctx.nccl_comm_init(world, rank, uid[0])
+        uid = dp.broadcast_bytes(ctx.nccl_unique_id() if rank == 0 else None)
+        comm = ctx.nccl_comm_init(world, rank, uid)
 
     nnz_hat = [g.nnz + g.n for g in pool]
 
@@ -282,13 +291,7 @@ def main():
     ctx.profile(False)
     ms = ev0.elapsed_time(ev1)
     torch.cuda.synchronize()
-    t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
-    t_work = torch.tensor([float(work)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t_work, op=dist.ReduceOp.SUM)
-    max_ms = float(t_ms.item())
-    total_work = float(t_work.item())
+    max_ms, total_work = dp.reduce_timing(ms, float(work), device=dev)
     value = total_work / (max_ms / 1e3)
 
     # ---- end to end: same calls, inputs copied from pinned host memory every step ----
@@ -336,16 +339,10 @@ def main():
             ework += step_e2e(i)
         e1.record(stream)
         stream.synchronize()
-        ems = e0.elapsed_time(e1)
-        t_e = torch.tensor([ems, float(ework)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t_e[:1], op=dist.ReduceOp.MAX)
-            tw = t_e[1:].clone()
-            dist.all_reduce(tw, op=dist.ReduceOp.SUM)
-            t_e[1] = tw[0]
-        e2e = {"value": float(t_e[1].item()) / (float(t_e[0].item()) / 1e3), "unit": UNIT,
+        ems, ework_all = dp.reduce_timing(e0.elapsed_time(e1), float(ework), device=dev)
+        e2e = {"value": ework_all / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
-               "ms_per_step": float(t_e[0].item()) / args.steps, "loss": float(loss_host.item())}
+               "ms_per_step": ems / args.steps, "loss": float(loss_host.item())}
 
     # ---- roofline of the dominant kernel (the SpMM, a2 + a7) ----
     peaks = load_peaks()
@@ -375,10 +372,11 @@ def main():
     # ---- CPU baseline: the oracle on host cores (rank 0, N = 1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, info = oracle_sample(cfg, pool[0], inputs[0], args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": "oracle",
-               "sample": f"rows [0,{info['rows']}) of the first subgraph, all {cfg.L} layers fwd+bwd + head, "
-                         f"fp64 plain loops, {info['seconds']:.1f} s"}
+        osamp = OracleSample(cfg, pool[0], inputs[0])
+        w_, dt_ = osamp.calibrate(args.cpu_seconds)
+        cpu = {"value": w_ / dt_, "unit": UNIT, "cores": osamp.cores(), "kind": "oracle",
+               "sample": f"rows [0,{osamp.rows}) of the first subgraph, all {cfg.L} layers fwd+bwd + head, "
+                         f"fp64 plain loops, {dt_:.1f} s"}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
