@@ -1,0 +1,139 @@
+"""Full-size parity: every BASELINE config's step, run exactly as bench.py runs it (GCNStep over
+the C ABI, same kernels, same launch configuration), checked against the fp64 oracle on
+sampled outputs (rows / columns the oracle computes one by one), stage-isolated:
+
+  a1  Â structure bit-exact, values within one fp32 rounding, valT = Alg. 4(val) bit-exact
+  a2  P_l rows (random + the heaviest rows)                   <= 1e-5  (fp32 SpMM)
+  a3  H_l rows from the GPU's P_l                              <= 5e-3  (TF32/BF16 GEMM)
+  a5  dW_l columns from the GPU's P_l and dZ_l                 <= 5e-3
+  a6+a7  dX_l rows = Âᵀ(dZ_l W_lᵀ) ⊙ gate, oracle T from GPU dZ <= 5e-3 (after a tensor-core GEMM)
+  a8  head loss / dS rows from the GPU's S                     <= 1e-5 relative
+plus bitwise run-to-run reproducibility of the whole step.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+import paper_2010_03166_b200 as gsg
+import workload as wl
+from paper_2010_03166_b200.step import GCNStep
+
+pytestmark = pytest.mark.gpu
+
+SPMM_TOL, GEMM_TOL = 1e-5, 5e-3
+
+
+def rel(gpu, ref):
+    gpu, ref = np.asarray(gpu, np.float64), np.asarray(ref, np.float64)
+    assert np.all(np.isfinite(gpu))
+    return float(np.abs(gpu - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def h(t):
+    torch.cuda.synchronize()
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = gsg.Context(0)
+    yield c
+    c.close()
+
+
+def run_config(ctx, cid):
+    cfg = wl.CONFIGS[cid]
+    g = wl.sample_subgraph(cfg)
+    inp = wl.make_inputs(cfg, g.n)
+    sg = ctx.upload(g.indptr, g.indices, validate=True)
+    step = GCNStep(ctx, cfg.dims, g.n, cfg.head, cfg.classes, cfg.precision, weights=inp.Ws, w_mlp=inp.W_mlp)
+    X = torch.zeros((g.n, wl.ld_for(cfg.dims[0])), device="cuda")[:, :cfg.dims[0]]
+    X.copy_(torch.from_numpy(inp.X))
+    labels = None if inp.labels is None else torch.from_numpy(inp.labels).cuda()
+    dH = None
+    if inp.dH is not None:
+        dH = torch.zeros((g.n, wl.ld_for(cfg.dims[-1])), device="cuda")[:, :cfg.dims[-1]]
+        dH.copy_(torch.from_numpy(inp.dH))
+    step.forward_backward(sg, X, labels=labels, dH_top=dH)
+    ctx.sync()
+    return cfg, g, inp, sg, step, X, labels, dH
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_config_step_sampled_parity(ctx, cid):
+    cfg, g, inp, sg, step, X, labels, dH_top = run_config(ctx, cid)
+    n, L, d = g.n, cfg.L, cfg.dims
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW_SELF)
+    # a1
+    ip, ix, v, vt = sg.download()
+    assert np.array_equal(ip, A.indptr) and np.array_equal(ix, A.idx)
+    np.testing.assert_allclose(v, A.val, rtol=2 ** -23, atol=0)
+    assert np.array_equal(vt.astype(np.float64), orc.transpose_alg4(orc.AHat(ip, ix, v.astype(np.float64))))
+    rng = np.random.default_rng(cid)
+    deg = np.diff(g.indptr)
+    rows = np.unique(np.concatenate([rng.choice(n, 48, replace=False), np.argsort(deg)[-8:]]))
+    bf = cfg.precision == "bf16"
+    for l in range(L):
+        X_in = inp.X.astype(np.float64) if l == 0 else h(step.H[l - 1][:n])
+        P = h(step.P[l][:n])
+        # a2: P rows = Â X rows (the oracle's gather definition, row by row)
+        Pref = np.stack([orc.spmm(A, X_in, int(i), int(i) + 1)[i] for i in rows])
+        assert rel(P[rows], Pref) <= SPMM_TOL, f"layer {l} P"
+        # a3: H rows from the GPU's P (bf16 configs read the bf16 copy of P)
+        Pin = h(step.Plp[l][:n]) if bf else P
+        Wl = inp.Ws[l].astype(np.float64)
+        Href = np.maximum(orc.gemm(Pin[rows], Wl), 0)
+        assert rel(h(step.H[l][:n])[rows], Href) <= GEMM_TOL, f"layer {l} H"
+    # backward: the gate applied to layer L's upstream gradient
+    if cfg.head != "none":
+        S = h(step.S[:n])
+        HL = h(step.H[L - 1][:n])
+        loss, _, dS = orc.head(S, inp.labels, cfg.head)
+        assert abs(float(step.loss.item()) - loss) <= 1e-5 * abs(loss)
+        assert rel(h(step.dS[:n])[rows], dS[rows]) <= 1e-5
+        dSg = h(step.dS[:n])
+        cols = rng.choice(cfg.classes, min(8, cfg.classes), replace=False)
+        assert rel(h(step.dWm)[:, cols], orc.gemm(HL, dSg[:, cols], transA=True)) <= GEMM_TOL
+        dZ_top = h(step.dHL[:n])
+        Wm = inp.W_mlp.astype(np.float64)
+        ref = np.where(HL[rows] > 0, orc.gemm(dSg[rows], Wm, transB=True), 0)
+        assert rel(dZ_top[rows], ref) <= GEMM_TOL
+    else:
+        dZ_top = np.where(h(step.H[L - 1][:n]) > 0, inp.dH.astype(np.float64), 0.0)
+    dZ = dZ_top
+    for l in range(L - 1, -1, -1):
+        P = h(step.Plp[l][:n]) if bf else h(step.P[l][:n])
+        dZin = dZ
+        if bf:  # the BF16 GEMMs read bf16 copies of dZ
+            dZin = torch.from_numpy(dZ.astype(np.float32)).bfloat16().double().numpy()
+        cols = rng.choice(d[l + 1], 16, replace=False)
+        assert rel(h(step.dW[l])[:, cols], orc.gemm(P, dZin[:, cols], transA=True)) <= GEMM_TOL, f"layer {l} dW"
+        # a6 + a7: dX = Âᵀ (dZ Wᵀ) ⊙ 1[H_{l-1} > 0] on sampled rows (scatter definition restricted
+        # to the sampled output rows: dX[j] = sum over stored (i, j, a) of a * T[i])
+        Wl = inp.Ws[l].astype(np.float64)
+        xrows = np.unique(np.concatenate([rows[:10], np.argsort(deg)[-2:]]))
+        src_of = np.repeat(np.arange(n), np.diff(A.indptr))      # row i of every stored (i, j, a)
+        hit = np.isin(A.idx, xrows)
+        need = np.unique(src_of[hit])
+        T = np.zeros((n, d[l]))
+        T[need] = orc.gemm(dZin[need], Wl, transB=True)
+        ref = np.zeros((n, d[l]))
+        np.add.at(ref, A.idx[hit], A.val[hit][:, None] * T[src_of[hit]])
+        ref = ref[xrows]
+        if l > 0:
+            ref = np.where(h(step.H[l - 1][:n])[xrows] > 0, ref, 0.0)
+        dX = h(step.dX[l][:n])
+        assert rel(dX[xrows], ref) <= GEMM_TOL, f"layer {l} dX"
+        dZ = dX  # premasked dZ of the layer below (the GPU's own)
+
+
+@pytest.mark.parametrize("cid", [2, 5])
+def test_step_bitwise_reproducible(ctx, cid):
+    cfg, g, inp, sg, step, X, labels, dH = run_config(ctx, cid)
+    first = [t.clone() for t in step.H + step.dX] + [step.grad_flat.clone(), step.loss.clone()]
+    step.forward_backward(sg, X, labels=labels, dH_top=dH)
+    ctx.sync()
+    second = step.H + step.dX + [step.grad_flat, step.loss]
+    for a, b in zip(first, second):
+        assert torch.equal(a, b)

@@ -21,22 +21,42 @@ __global__ void k_stream(const float4* __restrict__ p, size_t n4, int passes, fl
   if (acc.x + acc.y + acc.z + acc.w == 12345.f) *out = acc.x;
 }
 
-// each warp: `iters` gathers of one 512-byte row chunk at a pseudo-random row, 8 in flight
+// each warp: `iters` gathers of a (W x 512)-byte row chunk at a pseudo-random row; U rows in flight
+template <int W, int U>
 __global__ void k_gather(const float4* __restrict__ slab, int rows, int ld4, int iters, float* out) {
   const int lane = threadIdx.x & 31;
   unsigned s = (blockIdx.x * blockDim.x + threadIdx.x) / 32 * 2654435761u + 12345u;
   float4 acc = make_float4(0, 0, 0, 0);
-  for (int it = 0; it < iters; it += 8) {
-    float4 v[8];
+  for (int it = 0; it < iters; it += U) {
+    float4 v[U][W];
 #pragma unroll
-    for (int u = 0; u < 8; u++) {
+    for (int u = 0; u < U; u++) {
       s = s * 1664525u + 1013904223u;
-      v[u] = __ldg(slab + (size_t)(s % rows) * ld4 + lane);
+#pragma unroll
+      for (int w = 0; w < W; w++) v[u][w] = __ldg(slab + (size_t)(s % rows) * ld4 + lane + 32 * w);
     }
 #pragma unroll
-    for (int u = 0; u < 8; u++) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
+    for (int u = 0; u < U; u++)
+#pragma unroll
+      for (int w = 0; w < W; w++) { acc.x += v[u][w].x; acc.y += v[u][w].y; acc.z += v[u][w].z; acc.w += v[u][w].w; }
   }
   if (acc.x + acc.y + acc.z + acc.w == 12345.f) *out = acc.x;
+}
+
+template <int W, int U>
+double gather_bw(const float4* buf, int rows, int ld4, int blocks, int threads, float* out) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int iters = 2048;
+  k_gather<W, U><<<blocks, threads>>>(buf, rows, ld4, 64, out);
+  cudaEventRecord(a);
+  k_gather<W, U><<<blocks, threads>>>(buf, rows, ld4, iters, out);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  return (double)blocks * (threads / 32) * iters * W * 512.0 / (ms / 1e3) / 1e9;
 }
 
 int main() {
@@ -63,17 +83,14 @@ int main() {
   cudaEventSynchronize(b);
   cudaEventElapsedTime(&ms, a, b);
   double l2_stream = (double)bytes * passes / (ms / 1e3) / 1e9;
-  // 2. gathers of 512-byte row chunks from a 10 MB slab (20000 rows x 128 fp32)
-  const int rows = 20000, ld4 = 32, iters = 4096;
-  const int blocks = sms * 8;
-  k_gather<<<blocks, 256>>>(buf, rows, ld4, 64, out);
-  cudaEventRecord(a);
-  k_gather<<<blocks, 256>>>(buf, rows, ld4, iters, out);
-  cudaEventRecord(b);
-  cudaEventSynchronize(b);
-  cudaEventElapsedTime(&ms, a, b);
-  double gathers = (double)blocks * 8 * iters;  // warps x iterations
-  double l2_gather = gathers * 512.0 / (ms / 1e3) / 1e9;
+  // 2. gathers of W x 512-byte row chunks from a 20000-row slab of 1024 fp32 columns (82 MB)
+  const int rows = 20000, ld4 = 256;
+  double g512 = gather_bw<1, 8>(buf, rows, ld4, sms * 8, 256, out);
+  double g1k = gather_bw<2, 8>(buf, rows, ld4, sms * 4, 256, out);
+  double g2k = gather_bw<4, 4>(buf, rows, ld4, sms * 4, 256, out);
+  double g4k = gather_bw<8, 2>(buf, rows, ld4, sms * 4, 256, out);
+  double g1k_lo = gather_bw<2, 4>(buf, rows, ld4, sms * 8, 256, out);
+  double l2_gather = g512;
   // 3. HBM streaming read (4 GB, one pass)
   size_t hb = (size_t)4 << 30;
   k_stream<<<sms * 8, 256>>>(buf, hb / 16, 1, out);
@@ -84,7 +101,8 @@ int main() {
   cudaEventElapsedTime(&ms, a, b);
   double hbm_read = (double)hb / (ms / 1e3) / 1e9;
   printf("{\"l2_bytes\": %d, \"sms\": %d, \"l2_stream_read_gbs\": %.1f, \"l2_gather512_gbs\": %.1f, "
+         "\"l2_gather1k_gbs\": %.1f, \"l2_gather2k_gbs\": %.1f, \"l2_gather4k_gbs\": %.1f, \"l2_gather1k_u4_occ8_gbs\": %.1f, "
          "\"hbm_stream_read_gbs\": %.1f, \"err\": \"%s\"}\n",
-         l2, sms, l2_stream, l2_gather, hbm_read, cudaGetErrorString(cudaGetLastError()));
+         l2, sms, l2_stream, l2_gather, g1k, g2k, g4k, g1k_lo, hbm_read, cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
