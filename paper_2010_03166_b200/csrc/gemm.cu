@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -124,30 +125,88 @@ struct GemmArgs {
   int accumulate;
   float* ws;        // split-K partials [splits][M][ldws]
   int64_t ldws;
+  int mpad;         // rows per split in ws (num_m * tile rows): TMA-stored partial tiles never straddle splits
+  int tma_store;    // 1: C / ws written by TMA bulk-tensor stores from swizzled smem staging
   uint32_t idesc;
 };
 
-template <int BN, bool BF16>
+// Per-CTA configuration. CTA2 = cta_group::2: a CTA pair computes a 256 x BN tile with one
+// tcgen05.mma (M = 256); each CTA stages its 128 rows of A and half (BN/2) of B, so per-SM
+// operand traffic per FLOP drops by a third vs. the 128 x BN single-CTA tile.
+template <int BN, bool BF16, bool CTA2>
 struct Cfg {
   static constexpr int ELEM = BF16 ? 2 : 4;
   static constexpr int BK = 128 / ELEM;             // one 128-byte swizzle row of K
   static constexpr int UMMA_K = 32 / ELEM;          // 8 (tf32) / 16 (bf16)
   static constexpr int MN_PER_ROW = 128 / ELEM;     // MN elements per 128B row (MN-major)
+  static constexpr int BMT = CTA2 ? 2 * BM : BM;    // tile rows (M) per CTA group
+  static constexpr int BNC = CTA2 ? BN / 2 : BN;    // B rows (N) staged per CTA
   static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_BYTES = BN * 128;
+  static constexpr int B_BYTES = BNC * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN >= 256 ? 4 : 6;
+  static constexpr int STAGES = STAGE_BYTES >= 48 * 1024 ? 4 : 6;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256 /*barriers*/;
+  static constexpr int STG_BYTES = 4 * 2 * 4096;     // 4 epilogue warps x 2 buffers x (32 x 32 fp32)
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 256 /*barriers*/;
 };
 
-template <int BN, bool BF16, bool A_MN, bool B_MN>
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA load whose completion is counted on the pair leader's mbarrier (cta_group::2)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+template <bool BF16>
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  if constexpr (BF16) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+
+template <int BN, bool BF16, bool A_MN, bool B_MN, bool CTA2>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const GemmArgs g) {
-  using C = Cfg<BN, BF16>;
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
+  using C = Cfg<BN, BF16, CTA2>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* stg = smem + C::STAGES * C::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + C::STG_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -156,67 +215,101 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int tiles = g.num_m * g.num_n * g.splits;
+  const uint32_t rank = CTA2 ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
+  const int group = CTA2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ngroups = CTA2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (g.tma_store) prefetch_tmap(&tmC);
     for (int s = 0; s < C::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CTA2 ? 8 : 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(C::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CTA2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CTA2) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (both CTAs of a pair) =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = group; t < tiles; t += ngroups) {
         const int per_split = g.num_m * g.num_n;
         const int s = t / per_split, r = t % per_split;
         const int mb = r / g.num_n, nb = r % g.num_n;
+        const int m0 = mb * C::BMT + (int)rank * BM;
+        const int n0 = nb * BN + (int)rank * C::BNC;
         const int kb0 = s * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
         for (int kb = kb0; kb < kb1; kb++) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
           const int k0 = kb * C::BK;
-          if constexpr (A_MN) {
+          if constexpr (CTA2) {
+            const uint32_t lb = map_to_rank(smem_u32(&full[stage]), 0);
+            if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            if constexpr (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / C::MN_PER_ROW; j++)
-              tma_load_2d(sa + j * (C::BK * 128), &tmA, &full[stage], mb * BM + j * C::MN_PER_ROW, k0);
-          } else {
-            tma_load_2d(sa, &tmA, &full[stage], k0, mb * BM);
-          }
-          if constexpr (B_MN) {
+              for (int j = 0; j < BM / C::MN_PER_ROW; j++)
+                tma_load_2d_pair(sa + j * (C::BK * 128), &tmA, lb, m0 + j * C::MN_PER_ROW, k0);
+            } else {
+              tma_load_2d_pair(sa, &tmA, lb, k0, m0);
+            }
+            if constexpr (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / C::MN_PER_ROW; j++)
-              tma_load_2d(sb + j * (C::BK * 128), &tmB, &full[stage], nb * BN + j * C::MN_PER_ROW, k0);
+              for (int j = 0; j < C::BNC / C::MN_PER_ROW; j++)
+                tma_load_2d_pair(sb + j * (C::BK * 128), &tmB, lb, n0 + j * C::MN_PER_ROW, k0);
+            } else {
+              tma_load_2d_pair(sb, &tmB, lb, k0, n0);
+            }
           } else {
-            tma_load_2d(sb, &tmB, &full[stage], k0, nb * BN);
+            mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            if constexpr (A_MN) {
+#pragma unroll
+              for (int j = 0; j < BM / C::MN_PER_ROW; j++)
+                tma_load_2d(sa + j * (C::BK * 128), &tmA, &full[stage], m0 + j * C::MN_PER_ROW, k0);
+            } else {
+              tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+            }
+            if constexpr (B_MN) {
+#pragma unroll
+              for (int j = 0; j < C::BNC / C::MN_PER_ROW; j++)
+                tma_load_2d(sb + j * (C::BK * 128), &tmB, &full[stage], n0 + j * C::MN_PER_ROW, k0);
+            } else {
+              tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+            }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
+    // ===================== MMA issuer (pair leader only) =====================
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = group; t < tiles; t += ngroups) {
         const int per_split = g.num_m * g.num_n;
         const int s = t / per_split;
         const int kb0 = s * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
@@ -235,44 +328,118 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             else ad = smem_desc<2>(a_addr + kk * 32, 16, 1024);
             if constexpr (B_MN) bd = mn_desc<BF16, C::BK>(b_addr, kk);
             else bd = smem_desc<2>(b_addr + kk * 32, 16, 1024);
-            tc_mma<BF16>(tmem_d, ad, bd, g.idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            const uint32_t en = (kb > kb0 || kk > 0) ? 1u : 0u;
+            if constexpr (CTA2) tc_mma_pair<BF16>(tmem_d, ad, bd, g.idesc, en);
+            else tc_mma<BF16>(tmem_d, ad, bd, g.idesc, en);
           }
-          tc_commit(&empty[stage]);
+          if constexpr (CTA2) tc_commit_pair(&empty[stage]);
+          else tc_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&tfull[acc]);
+        if constexpr (CTA2) tc_commit_pair(&tfull[acc]);
+        else tc_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue =====================
+    // ===================== epilogue (own 128 rows of the tile) =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t tempty_leader = CTA2 ? map_to_rank(smem_u32(&tempty[0]), 0) : 0u;
+    int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (int t = group; t < tiles; t += ngroups) {
       const int per_split = g.num_m * g.num_n;
       const int s = t / per_split, r = t % per_split;
       const int mb = r / g.num_n, nb = r % g.num_n;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = mb * BM + q * 32 + lane;
+      const int row_base = mb * C::BMT + (int)rank * BM + q * 32;
+      const int row = row_base + lane;
       const bool row_ok = row < g.M;
       for (int c = 0; c < BN / 32; c++) {
         uint32_t v[32];
         __syncwarp();
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
         const int col0 = nb * BN + c * 32;
+        if (g.tma_store) {
+          if (row_base >= g.M || col0 >= g.N) continue;  // warp-uniform: block fully outside C
+          float x[32];
+#pragma unroll
+          for (int i = 0; i < 32; i++) x[i] = __uint_as_float(v[i]);
+          if (g.splits == 1) {
+            if (g.epi == GSG_EPI_RELU) {
+#pragma unroll
+              for (int i = 0; i < 32; i++) x[i] = fmaxf(x[i], 0.f);
+            } else if (g.epi == GSG_EPI_MASK && row_ok) {
+              const float* ax = g.aux + (int64_t)row * g.ldaux + col0;
+              if (col0 + 32 <= g.N) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  const float4 m = __ldg(reinterpret_cast<const float4*>(ax + i));
+                  x[i] = m.x > 0.f ? x[i] : 0.f;
+                  x[i + 1] = m.y > 0.f ? x[i + 1] : 0.f;
+                  x[i + 2] = m.z > 0.f ? x[i + 2] : 0.f;
+                  x[i + 3] = m.w > 0.f ? x[i + 3] : 0.f;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; i++) if (col0 + i < g.N) x[i] = ax[i] > 0.f ? x[i] : 0.f;
+              }
+            }
+            if (g.Clp && row_ok) {
+              __nv_bfloat16* dl = g.Clp + (int64_t)row * g.ldclp + col0;
+              if (col0 + 32 <= g.N) {
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                  __nv_bfloat162 p0 = __floats2bfloat162_rn(x[i], x[i + 1]);
+                  __nv_bfloat162 p1 = __floats2bfloat162_rn(x[i + 2], x[i + 3]);
+                  __nv_bfloat162 p2 = __floats2bfloat162_rn(x[i + 4], x[i + 5]);
+                  __nv_bfloat162 p3 = __floats2bfloat162_rn(x[i + 6], x[i + 7]);
+                  uint4 u;
+                  u.x = *reinterpret_cast<uint32_t*>(&p0);
+                  u.y = *reinterpret_cast<uint32_t*>(&p1);
+                  u.z = *reinterpret_cast<uint32_t*>(&p2);
+                  u.w = *reinterpret_cast<uint32_t*>(&p3);
+                  *reinterpret_cast<uint4*>(dl + i) = u;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; i++) if (col0 + i < g.N) dl[i] = __float2bfloat16_rn(x[i]);
+              }
+            }
+          }
+          // stage the 32 x 32 block (128B-swizzled rows) and store it with one TMA bulk-tensor op
+          uint8_t* buf = stg + (q * 2 + sbuf) * 4096;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            const int crow = g.splits > 1 ? s * g.mpad + row_base : row_base;
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tmC)),
+                         "r"(col0), "r"(crow), "r"(smem_u32(buf))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          sbuf ^= 1;
+          continue;
+        }
         if (!row_ok || col0 >= g.N) continue;
         float x[32];
 #pragma unroll
         for (int i = 0; i < 32; i++) x[i] = __uint_as_float(v[i]);
         if (g.splits > 1) {
-          float* dst = g.ws + ((int64_t)s * g.M + row) * g.ldws + col0;
+          float* dst = g.ws + ((int64_t)s * g.mpad + row) * g.ldws + col0;
           if (col0 + 32 <= g.N) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
           } else {
-            
 #pragma unroll
             for (int i = 0; i < 32; i++) if (col0 + i < g.N) dst[i] = x[i];
           }
@@ -288,7 +455,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               x[i] += o.x; x[i + 1] += o.y; x[i + 2] += o.z; x[i + 3] += o.w;
             }
           } else {
-            
 #pragma unroll
             for (int i = 0; i < 32; i++) if (col0 + i < g.N) x[i] += dst[i];
           }
@@ -308,7 +474,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               x[i + 3] = m.w > 0.f ? x[i + 3] : 0.f;
             }
           } else {
-            
 #pragma unroll
             for (int i = 0; i < 32; i++) if (col0 + i < g.N) x[i] = ax[i] > 0.f ? x[i] : 0.f;
           }
@@ -317,9 +482,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(x[i], x[i + 1], x[i + 2], x[i + 3]);
         } else {
-          
 #pragma unroll
-            for (int i = 0; i < 32; i++) if (col0 + i < g.N) dst[i] = x[i];
+          for (int i = 0; i < 32; i++) if (col0 + i < g.N) dst[i] = x[i];
         }
         if (g.Clp) {
           __nv_bfloat16* dl = g.Clp + (int64_t)row * g.ldclp + col0;
@@ -338,7 +502,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               *reinterpret_cast<uint4*>(dl + i) = u;
             }
           } else {
-            
 #pragma unroll
             for (int i = 0; i < 32; i++) if (col0 + i < g.N) dl[i] = __float2bfloat16_rn(x[i]);
           }
@@ -346,16 +509,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CTA2) mbar_arrive_cluster(tempty_leader + acc * 8);
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (g.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CTA2) cluster_sync_all();
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
-                 : "memory");
+    if constexpr (CTA2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -369,7 +541,7 @@ __global__ void k_splitk_reduce(GemmArgs g) {
     float x[4] = {0.f, 0.f, 0.f, 0.f};
     const int w = min(4, g.N - c);
     for (int s = 0; s < g.splits; s++) {
-      const float* p = g.ws + ((int64_t)s * g.M + row) * g.ldws + c;
+      const float* p = g.ws + ((int64_t)s * g.mpad + row) * g.ldws + c;
       if (w == 4) {
         const float4 v = *reinterpret_cast<const float4*>(p);
         x[0] += v.x; x[1] += v.y; x[2] += v.z; x[3] += v.w;
@@ -448,29 +620,63 @@ int make_map(CUtensorMap* m, const void* base, bool bf16, int64_t rows, int64_t 
   return GSG_OK;
 }
 
-template <int BN, bool BF16, bool A_MN, bool B_MN>
-int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& g) {
-  using C = Cfg<BN, BF16>;
-  auto kern = k_gemm<BN, BF16, A_MN, B_MN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    GSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    attr_set = true;
-  }
-  const int tiles = g.num_m * g.num_n * g.splits;
-  const int grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
-  kern<<<grid, kGemmThreads, C::SMEM, ctx->stream>>>(ma, mb, g);
-  count_launch(ctx);
-  GSG_CUDA(cudaGetLastError());
+// fp32 [rows x cols] store map, box 32 x 32, 128B swizzle (matches the epilogue staging layout)
+int make_store_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(GSG_EINVAL, "cuTensorMapEncodeTiled(store) failed (%d): rows=%lld cols=%lld ld=%lld", (int)r,
+                (long long)rows, (long long)cols, (long long)ld);
   return GSG_OK;
 }
 
-template <int BN, bool BF16>
-int dispatch_major(gsg_ctx* ctx, bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& g) {
-  if (!a_mn && !b_mn) return run_gemm<BN, BF16, false, false>(ctx, ma, mb, g);
-  if (!a_mn && b_mn) return run_gemm<BN, BF16, false, true>(ctx, ma, mb, g);
-  if (a_mn && !b_mn) return run_gemm<BN, BF16, true, false>(ctx, ma, mb, g);
-  return run_gemm<BN, BF16, true, true>(ctx, ma, mb, g);
+template <int BN, bool BF16, bool A_MN, bool B_MN, bool CTA2>
+int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const GemmArgs& g) {
+  using C = Cfg<BN, BF16, CTA2>;
+  auto kern = k_gemm<BN, BF16, A_MN, B_MN, CTA2>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    GSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    if (CTA2) GSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    attr_set = true;
+  }
+  const int tiles = g.num_m * g.num_n * g.splits;
+  int grid;
+  if (CTA2) {
+    const int pairs = ctx->num_sms / 2;
+    grid = 2 * (tiles < pairs ? tiles : pairs);
+  } else {
+    grid = tiles < ctx->num_sms ? tiles : ctx->num_sms;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CTA2 ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, g));
+  count_launch(ctx);
+  return GSG_OK;
+}
+
+template <int BN, bool BF16, bool CTA2>
+int dispatch_major(gsg_ctx* ctx, bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
+                   const CUtensorMap& mc, const GemmArgs& g) {
+  if (!a_mn && !b_mn) return run_gemm<BN, BF16, false, false, CTA2>(ctx, ma, mb, mc, g);
+  if (!a_mn && b_mn) return run_gemm<BN, BF16, false, true, CTA2>(ctx, ma, mb, mc, g);
+  if (a_mn && !b_mn) return run_gemm<BN, BF16, true, false, CTA2>(ctx, ma, mb, mc, g);
+  return run_gemm<BN, BF16, true, true, CTA2>(ctx, ma, mb, mc, g);
 }
 
 }  // namespace
@@ -514,8 +720,12 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   int rc = get_encode();
   if (rc) return rc;
   const int BN = N <= 128 ? 128 : 256;
+  // pair (cta_group::2, 256-row tiles) whenever the shape fills the pair tile; GSG_GEMM_1CTA=1 forces 1-CTA
+  static const bool force1 = getenv("GSG_GEMM_1CTA") && atoi(getenv("GSG_GEMM_1CTA")) == 1;
+  const bool cta2 = !force1 && BN == 256 && M > BM;
+  const int BMT = cta2 ? 2 * BM : BM;
   const int BK = 128 / elem, mnrow = 128 / elem;
-  g.num_m = (M + BM - 1) / BM;
+  g.num_m = (M + BMT - 1) / BMT;
   g.num_n = (N + BN - 1) / BN;
   g.num_kb = (K + BK - 1) / BK;
   const int base_tiles = g.num_m * g.num_n;
@@ -532,26 +742,42 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   if (splits > g.num_kb) splits = g.num_kb;
   g.kb_per_split = (g.num_kb + splits - 1) / splits;
   g.splits = (g.num_kb + g.kb_per_split - 1) / g.kb_per_split;  // no empty split
+  g.mpad = g.num_m * BMT;
   if (g.splits > 1) {
-    g.ldws = (N + 3) / 4 * 4;
-    rc = ctx->ws_splitk.reserve((size_t)g.splits * M * g.ldws * sizeof(float));
+    g.ldws = (N + 7) / 8 * 8;
+    rc = ctx->ws_splitk.reserve((size_t)g.splits * g.mpad * g.ldws * sizeof(float));
     if (rc) return rc;
     g.ws = static_cast<float*>(ctx->ws_splitk.ptr);
   }
   // instruction descriptor: D=F32, A/B = TF32 (2) or BF16 (1), majorness, N>>3, M>>4
   const uint32_t fmt = bf16 ? 1u : 2u;
   g.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(transA ? 1 : 0) << 15) |
-            ((uint32_t)(transB ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+            ((uint32_t)(transB ? 0 : 1) << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BMT >> 4) << 24);
+  const int BNC = cta2 ? BN / 2 : BN;  // B rows staged per CTA
   CUtensorMap ma, mb;
   if (transA) rc = make_map(&ma, A, bf16, K, M, lda, mnrow, BK, true);   // MN-major A (stored K x M)
   else rc = make_map(&ma, A, bf16, M, K, lda, BK, BM, false);            // K-major A (stored M x K)
   if (rc) return rc;
-  if (transB) rc = make_map(&mb, B, bf16, N, K, ldb, BK, BN, false);     // K-major B (stored N x K)
+  if (transB) rc = make_map(&mb, B, bf16, N, K, ldb, BK, BNC, false);    // K-major B (stored N x K)
   else rc = make_map(&mb, B, bf16, K, N, ldb, mnrow, BK, true);          // MN-major B (stored K x N)
   if (rc) return rc;
+  // epilogue store map: C itself, or the split-K workspace [splits * mpad x ldws]
+  CUtensorMap mc;
+  g.tma_store = accumulate ? 0 : 1;
+  if (g.splits > 1) rc = make_store_map(&mc, g.ws, (int64_t)g.splits * g.mpad, N, g.ldws);
+  else rc = make_store_map(&mc, Cp, M, N, ldc);
+  if (rc) return rc;
   const bool a_mn = transA, b_mn = !transB;
-  if (bf16) rc = BN == 128 ? dispatch_major<128, true>(ctx, a_mn, b_mn, ma, mb, g) : dispatch_major<256, true>(ctx, a_mn, b_mn, ma, mb, g);
-  else rc = BN == 128 ? dispatch_major<128, false>(ctx, a_mn, b_mn, ma, mb, g) : dispatch_major<256, false>(ctx, a_mn, b_mn, ma, mb, g);
+  if (cta2) {
+    rc = bf16 ? dispatch_major<256, true, true>(ctx, a_mn, b_mn, ma, mb, mc, g)
+              : dispatch_major<256, false, true>(ctx, a_mn, b_mn, ma, mb, mc, g);
+  } else if (bf16) {
+    rc = BN == 128 ? dispatch_major<128, true, false>(ctx, a_mn, b_mn, ma, mb, mc, g)
+                   : dispatch_major<256, true, false>(ctx, a_mn, b_mn, ma, mb, mc, g);
+  } else {
+    rc = BN == 128 ? dispatch_major<128, false, false>(ctx, a_mn, b_mn, ma, mb, mc, g)
+                   : dispatch_major<256, false, false>(ctx, a_mn, b_mn, ma, mb, mc, g);
+  }
   if (rc) return rc;
   if (g.splits > 1) {
     int64_t total = (int64_t)M * ((N + 3) / 4);
