@@ -74,7 +74,12 @@ enum {
 enum {
   GSG_NO_RELU = 1,         /* forward: H = P W (no ReLU)                                   */
   GSG_DH_PREMASKED = 2,    /* backward: dH already equals dZ = dH ⊙ 1[H>0] (fused upstream) */
-  GSG_ACCUM_DW = 4         /* backward: dW += Pᵀ dZ instead of dW = Pᵀ dZ                  */
+  GSG_ACCUM_DW = 4,        /* backward: dW += Pᵀ dZ instead of dW = Pᵀ dZ                  */
+  GSG_ORDER_A_XW = 8       /* chain order 2 of §7.1: forward Y = X W then
+                              H = ReLU(Â Y) (the SpMM runs at width f_out); backward
+                              G = Âᵀ dZ, dW = Xᵀ G, dX = (G Wᵀ) ⊙ 1[H_below > 0]. With this
+                              flag the P arguments of both calls carry X's role: forward
+                              writes Y (n x f_out) into P; backward reads X (n x f_in) from P. */
 };
 
 /* ---- GEMM epilogues (gsg_gemm) ------------------------------------------------------- */

@@ -28,7 +28,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 GSG_OK, GSG_EINVAL, GSG_EGRAPH, GSG_ENOMEM, GSG_ECUDA, GSG_ENCCL, GSG_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 GSG_NORM_ROW_SELF, GSG_NORM_SYM_SELF, GSG_NORM_ROW, GSG_NORM_VALUES = 0, 1, 2, 3
 GSG_PREC_TF32, GSG_PREC_BF16 = 0, 1
-GSG_NO_RELU, GSG_DH_PREMASKED, GSG_ACCUM_DW = 1, 2, 4
+GSG_NO_RELU, GSG_DH_PREMASKED, GSG_ACCUM_DW, GSG_ORDER_A_XW = 1, 2, 4, 8
 GSG_EPI_NONE, GSG_EPI_RELU, GSG_EPI_MASK = 0, 1, 2
 GSG_HEAD_SOFTMAX, GSG_HEAD_SIGMOID = 0, 1
 GSG_K_SPMM, GSG_K_GEMM, GSG_K_NORM, GSG_K_OTHER = 0, 1, 2, 3
@@ -138,9 +138,12 @@ class Subgraph:
         check(gsg_subgraph_download(self.ctx.h, self.h, ip.ctypes.data, ix.ctypes.data, v.ctypes.data, vt.ctypes.data))
         return ip, ix[:nh], v[:nh], vt[:nh]
 
-    def assign(self, n: int, nnz: int, indptr_ptr: int, indices_ptr: int, values_ptr: int = 0, validate=False):
-        """Refill from host arrays given as raw pointers (pinned memory -> async copies)."""
-        check(gsg_subgraph_assign(self.ctx.h, self.h, n, nnz, indptr_ptr, indices_ptr or None, values_ptr or None,
+    def assign(self, n: int, nnz: int, indptr_ptr: int, indices_ptr: int, values_ptr: int = 0, validate=False,
+               ctx: "Context | None" = None):
+        """Refill from host arrays given as raw pointers (pinned memory -> async copies), on the
+        stream of `ctx` (default: the owning context), e.g. a copy stream overlapping compute."""
+        c = self.ctx if ctx is None else ctx
+        check(gsg_subgraph_assign(c.h, self.h, n, nnz, indptr_ptr, indices_ptr or None, values_ptr or None,
                                   int(validate)))
         self.n, self.nnz = n, nnz
         return self

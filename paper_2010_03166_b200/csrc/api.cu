@@ -411,10 +411,30 @@ GSG_API int gsg_layer_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   GSG_CHECK(f_in >= 1 && f_out >= 1, GSG_EINVAL, "f_in=%d f_out=%d must be >= 1", f_in, f_out);
   GSG_CHECK(W && ldw >= f_out, GSG_EINVAL, "W NULL or ldw < f_out");
-  GSG_CHECK(precision != GSG_PREC_BF16 || Plp, GSG_EINVAL, "BF16 forward needs the bf16 P copy (Plp)");
+  GSG_CHECK(precision != GSG_PREC_BF16 || Plp || (flags & GSG_ORDER_A_XW), GSG_EINVAL,
+            "BF16 forward needs the bf16 P copy (Plp)");
   DeviceGuard dg(c->device);
   const int n = sg->n;
-  int rc = spmm_launch(c, sg, 0, f_in, X, ldx, P, ldp, precision == GSG_PREC_BF16 ? Plp : nullptr, ldplp, nullptr, 0);
+  int rc;
+  if (flags & GSG_ORDER_A_XW) {
+    // chain order 2 (§7.1): Y = X W (into P), H = ReLU(Â Y)
+    GSG_CHECK(ldp >= f_out, GSG_EINVAL, "GSG_ORDER_A_XW: P holds Y = X W and needs ldp >= f_out");
+    if (precision == GSG_PREC_BF16) {
+      const int64_t ldwl = round_up(f_out, 8), ldxl = round_up(f_in, 8);
+      if ((rc = c->ws_lp0.reserve(sizeof(uint16_t) * f_in * ldwl))) return rc;
+      if ((rc = c->ws_lp2.reserve(sizeof(uint16_t) * n * ldxl))) return rc;
+      if ((rc = to_bf16_launch(c, f_in, f_out, W, ldw, c->ws_lp0.ptr, ldwl))) return rc;
+      if ((rc = to_bf16_launch(c, n, f_in, X, ldx, c->ws_lp2.ptr, ldxl))) return rc;
+      rc = gemm_launch(c, n, f_out, f_in, c->ws_lp2.ptr, ldxl, 0, c->ws_lp0.ptr, ldwl, 0, P, ldp, nullptr, 0, precision,
+                       GSG_EPI_NONE, nullptr, 0, 0, 0);
+    } else {
+      rc = gemm_launch(c, n, f_out, f_in, X, ldx, 0, W, ldw, 0, P, ldp, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0,
+                       0, 0);
+    }
+    if (rc) return rc;
+    return spmm_launch(c, sg, 0, f_out, P, ldp, H, ldh, Hlp, ldhlp, nullptr, 0, (flags & GSG_NO_RELU) ? 0 : 1);
+  }
+  rc = spmm_launch(c, sg, 0, f_in, X, ldx, P, ldp, precision == GSG_PREC_BF16 ? Plp : nullptr, ldplp, nullptr, 0);
   if (rc) return rc;
   const int epi = (flags & GSG_NO_RELU) ? GSG_EPI_NONE : GSG_EPI_RELU;
   if (precision == GSG_PREC_BF16) {
@@ -465,6 +485,31 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
     if ((rc = c->ws_lp1.reserve(sizeof(uint16_t) * n * lddzlp))) return rc;
     if ((rc = to_bf16_launch(c, n, f_out, dH, lddh, c->ws_lp1.ptr, lddzlp))) return rc;
     dZlp = c->ws_lp1.ptr;
+  }
+  if (flags & GSG_ORDER_A_XW) {
+    // chain order 2 backward: G = Âᵀ dZ (width f_out), dW = Xᵀ G, dX = (G Wᵀ) ⊙ 1[H_below > 0]; P holds X
+    const int64_t ldg = round_up(f_out, 8);
+    if ((rc = c->ws_T.reserve(sizeof(float) * n * ldg))) return rc;
+    float* G = (float*)c->ws_T.ptr;
+    void* Glp = nullptr;
+    if (bf16) {
+      if ((rc = c->ws_lp2.reserve(sizeof(uint16_t) * n * ldg))) return rc;
+      Glp = c->ws_lp2.ptr;
+    }
+    if ((rc = spmm_launch(c, sg, 1, f_out, dZ, lddz, G, ldg, Glp, ldg, nullptr, 0))) return rc;
+    const void* Wop2 = W;
+    int64_t ldw2 = ldw;
+    if (bf16) {
+      ldw2 = round_up(f_out, 8);
+      if ((rc = c->ws_lp0.reserve(sizeof(uint16_t) * f_in * ldw2))) return rc;
+      if ((rc = to_bf16_launch(c, f_in, f_out, W, ldw, c->ws_lp0.ptr, ldw2))) return rc;
+      Wop2 = c->ws_lp0.ptr;
+    }
+    rc = gemm_launch(c, f_in, f_out, n, bf16 ? Plp : (const void*)P, bf16 ? ldplp : ldp, 1, bf16 ? Glp : (const void*)G,
+                     ldg, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, (flags & GSG_ACCUM_DW) ? 1 : 0);
+    if (rc || !dX) return rc;
+    return gemm_launch(c, n, f_in, f_out, bf16 ? Glp : (const void*)G, ldg, 0, Wop2, ldw2, 1, dX, lddx, dXlp, lddxlp,
+                       precision, Hbelow ? GSG_EPI_MASK : GSG_EPI_NONE, Hbelow, ldhb, 0, 0);
   }
   const void* Wop = W;
   int64_t ldwop = ldw;

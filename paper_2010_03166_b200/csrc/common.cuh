@@ -131,7 +131,7 @@ struct ProfScope {
 // launch wrappers implemented in the .cu files
 int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode);
 int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, const float* X, int64_t ldx,
-                float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm);
+                float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, int relu = 0);
 int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA,
                 const void* B, int64_t ldb, int transB, float* C, int64_t ldc, void* Clp, int64_t ldclp,
                 int precision, int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate);

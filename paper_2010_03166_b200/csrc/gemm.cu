@@ -731,12 +731,21 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   const int base_tiles = g.num_m * g.num_n;
   int splits = split_k;
   if (splits <= 0) {
+    // Pick the K split that minimizes modeled time: waves x (k-blocks per split + epilogue
+    // overhead of ~2 k-blocks) + the fixed-order reduction (reads s partials, writes C).
+    const int units = cta2 ? ctx->num_sms / 2 : ctx->num_sms;
+    const double t_kb_us = cta2 ? 0.52 : 0.55;                 // one k-block of one tile (TF32)
+    const double red_us_per_split = (double)M * N * 4.0 / 5.0e6;  // ~5 TB/s streaming
+    int max_s = g.num_kb / 4;                                   // keep >= 4 k-blocks per split
+    if (max_s > 64) max_s = 64;
+    if (max_s < 1) max_s = 1;
+    double best = 1e30;
     splits = 1;
-    if (base_tiles < ctx->num_sms / 2) {
-      splits = ctx->num_sms / base_tiles;
-      int max_s = g.num_kb / 4;  // keep >= 4 k-blocks per split
-      if (splits > max_s) splits = max_s;
-      if (splits < 1) splits = 1;
+    for (int s = 1; s <= max_s; s++) {
+      const int kbps = (g.num_kb + s - 1) / s;
+      const int waves = (base_tiles * s + units - 1) / units;
+      const double t = waves * (kbps + 2) * t_kb_us + (s > 1 ? (s + 1) * red_us_per_split : 0.0);
+      if (t < best * 0.97) { best = t; splits = s; }
     }
   }
   if (splits > g.num_kb) splits = g.num_kb;

@@ -40,6 +40,7 @@ struct SpmmArgs {
   uint2* __restrict__ Ylp;   // 4 bf16 per uint2
   int64_t ldylp4;
   const float4* __restrict__ mask;
+  int relu;                  // epilogue ReLU (chain order 2 forward: H = ReLU(Â (X W)))
   int64_t ldm4;
   const int32_t* __restrict__ perm;
   const int32_t* __restrict__ n_heavy_ptr;
@@ -167,6 +168,12 @@ __device__ __forceinline__ float4 group_row_sum(const SpmmArgs& a, int b, int e,
 }
 
 __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int c4, float4 acc) {
+  if (a.relu) {
+    acc.x = fmaxf(acc.x, 0.f);
+    acc.y = fmaxf(acc.y, 0.f);
+    acc.z = fmaxf(acc.z, 0.f);
+    acc.w = fmaxf(acc.w, 0.f);
+  }
   if (a.mask) {
     const float4 m = __ldg(a.mask + (int64_t)row * a.ldm4 + c4);
     acc.x = m.x > 0.f ? acc.x : 0.f;
@@ -313,7 +320,7 @@ int launch_k(gsg_ctx* ctx, K kern, int* occ_cache, const SpmmArgs& a, int64_t wa
 }  // namespace
 
 int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, const float* X, int64_t ldx,
-                float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm) {
+                float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, int relu) {
   GSG_CHECK(sg->norm_mode >= 0, GSG_EINVAL, "subgraph not normalized (call gsg_subgraph_normalize)");
   GSG_CHECK(f >= 1, GSG_EINVAL, "f must be >= 1 (got %d)", f);
   GSG_CHECK(X && Y, GSG_EINVAL, "X and Y must be non-NULL");
@@ -345,6 +352,7 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   a.Ylp = reinterpret_cast<uint2*>(Ylp);
   a.ldylp4 = ldylp / 4;
   a.mask = reinterpret_cast<const float4*>(mask);
+  a.relu = relu;
   a.ldm4 = ldm / 4;
   a.perm = sg->perm;
   a.n_heavy_ptr = sg->counters + kBins;

@@ -16,8 +16,14 @@ from __future__ import annotations
 
 import torch
 
-from . import (GSG_DH_PREMASKED, GSG_HEAD_SIGMOID, GSG_HEAD_SOFTMAX, GSG_NORM_ROW_SELF, GSG_PREC_BF16,
-               GSG_PREC_TF32, Context, Subgraph)
+from . import (GSG_DH_PREMASKED, GSG_HEAD_SIGMOID, GSG_HEAD_SOFTMAX, GSG_NORM_ROW_SELF, GSG_ORDER_A_XW,
+               GSG_PREC_BF16, GSG_PREC_TF32, Context, Subgraph)
+
+
+def chain_order(f_in: int, f_out: int) -> int:
+    """§7.1: (Â X) W costs δn²·f_in + n·f_in·f_out MACs, Â (X W) costs δn²·f_out +
+    n·f_in·f_out; order 2 iff f_in > f_out. Ties keep order 1 (equal MACs; the north star's order)."""
+    return 2 if f_in > f_out else 1
 
 
 def ld_for(f: int, align: int = 8) -> int:
@@ -31,9 +37,10 @@ def padded(rows: int, f: int, dtype=torch.float32, align: int = 8, device="cuda"
 
 class GCNStep:
     def __init__(self, ctx: Context, dims: list, n_max: int, head: str = "none", classes: int = 0,
-                 precision: str = "tf32", device: int = 0, weights=None, w_mlp=None):
+                 precision: str = "tf32", device: int = 0, weights=None, w_mlp=None, order: str = "auto"):
         self.ctx, self.dims, self.n_max = ctx, list(dims), n_max
         self.L = len(dims) - 1
+        self.order = [chain_order(dims[l], dims[l + 1]) if order == "auto" else int(order) for l in range(self.L)]
         self.head = head
         self.C = classes
         self.prec = GSG_PREC_BF16 if precision == "bf16" else GSG_PREC_TF32
@@ -43,7 +50,8 @@ class GCNStep:
         if weights is not None:
             for w, src in zip(self.W, weights):
                 w.copy_(torch.as_tensor(src))
-        self.P = [padded(n_max, dims[l], device=dev) for l in range(self.L)]
+        # order 1 keeps P = Â X (n x f_in); order 2 keeps Y = X W (n x f_out) in the same slot
+        self.P = [padded(n_max, dims[l + 1] if self.order[l] == 2 else dims[l], device=dev) for l in range(self.L)]
         self.H = [padded(n_max, dims[l + 1], device=dev) for l in range(self.L)]
         self.dX = [padded(n_max, dims[l], device=dev) for l in range(self.L)]
         self.Plp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
@@ -76,9 +84,13 @@ class GCNStep:
         if normalize:
             sg.normalize(GSG_NORM_ROW_SELF)
         h = X
+        inputs = []
         for l in range(self.L):
+            inputs.append(h)
+            o2 = self.order[l] == 2
             ctx.layer_forward(sg, h, self.W[l], self.P[l][:n], self.H[l][:n], d[l], d[l + 1], precision=self.prec,
-                              Plp=None if self.Plp[l] is None else self.Plp[l][:n])
+                              Plp=None if (self.Plp[l] is None or o2) else self.Plp[l][:n],
+                              flags=GSG_ORDER_A_XW if o2 else 0)
             h = self.H[l][:n]
         if self.head != "none":
             kind = GSG_HEAD_SOFTMAX if self.head == "softmax" else GSG_HEAD_SIGMOID
@@ -89,10 +101,15 @@ class GCNStep:
             dH, dHlp, flags = dH_top, None, 0
         for l in range(self.L - 1, -1, -1):
             Hb = self.H[l - 1][:n] if l > 0 else None
-            ctx.layer_backward(sg, self.P[l][:n], self.H[l][:n], dH, self.W[l], self.dW[l], self.dX[l][:n],
-                               d[l], d[l + 1], precision=self.prec,
-                               Plp=None if self.Plp[l] is None else self.Plp[l][:n], dHlp=dHlp,
-                               dXlp=None if self.dXlp[l] is None else self.dXlp[l][:n], H_below=Hb, flags=flags)
+            o2 = self.order[l] == 2
+            Pl = inputs[l] if o2 else self.P[l][:n]   # order 2 differentiates through X W: needs X
+            Plp = None if self.Plp[l] is None else self.Plp[l][:n]
+            if o2 and Plp is not None:
+                ctx.to_bf16(inputs[l], Plp)
+            ctx.layer_backward(sg, Pl, self.H[l][:n], dH, self.W[l], self.dW[l], self.dX[l][:n],
+                               d[l], d[l + 1], precision=self.prec, Plp=Plp, dHlp=dHlp,
+                               dXlp=None if self.dXlp[l] is None else self.dXlp[l][:n], H_below=Hb,
+                               flags=flags | (GSG_ORDER_A_XW if o2 else 0))
             dH = self.dX[l][:n]
             dHlp = None if self.dXlp[l] is None else self.dXlp[l][:n]
             flags = GSG_DH_PREMASKED  # the transposed aggregation already applied layer l-1's ReLU' gate
@@ -101,8 +118,9 @@ class GCNStep:
         return self.loss
 
     def work_edge_features(self, nnz_hat: int) -> int:
-        """2 * nnz' * f_in edge-features per layer (a2 + a7), summed over layers."""
-        return sum(2 * nnz_hat * self.dims[l] for l in range(self.L))
+        """2 * nnz' * f edge-features per layer (a2 + a7), summed over layers, where f is
+        the width the aggregation runs at: f_in under order 1, f_out under order 2."""
+        return sum(2 * nnz_hat * (self.dims[l + 1] if self.order[l] == 2 else self.dims[l]) for l in range(self.L))
 
     def gemm_flops(self, n: int) -> int:
         f = 6 * sum(n * self.dims[l] * self.dims[l + 1] for l in range(self.L))

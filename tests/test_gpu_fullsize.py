@@ -76,6 +76,14 @@ def test_config_step_sampled_parity(ctx, cid):
     bf = cfg.precision == "bf16"
     for l in range(L):
         X_in = inp.X.astype(np.float64) if l == 0 else h(step.H[l - 1][:n])
+        if step.order[l] == 2:
+            # chain order 2 (§7.1): Y = X W (GEMM), H = ReLU(Â Y) (SpMM)
+            Y = h(step.P[l][:n])
+            Wl = inp.Ws[l].astype(np.float64)
+            assert rel(Y[rows], orc.gemm(X_in[rows], Wl)) <= GEMM_TOL, f"layer {l} Y"
+            Href = np.stack([np.maximum(orc.spmm(A, Y, int(i), int(i) + 1)[i], 0) for i in rows])
+            assert rel(h(step.H[l][:n])[rows], Href) <= SPMM_TOL, f"layer {l} H (order 2)"
+            continue
         P = h(step.P[l][:n])
         # a2: P rows = Â X rows (the oracle's gather definition, row by row)
         Pref = np.stack([orc.spmm(A, X_in, int(i), int(i) + 1)[i] for i in rows])
@@ -103,7 +111,11 @@ def test_config_step_sampled_parity(ctx, cid):
         dZ_top = np.where(h(step.H[L - 1][:n]) > 0, inp.dH.astype(np.float64), 0.0)
     dZ = dZ_top
     for l in range(L - 1, -1, -1):
-        P = h(step.Plp[l][:n]) if bf else h(step.P[l][:n])
+        if step.order[l] == 2:  # dW = Xᵀ (Âᵀ dZ) = (Â X)ᵀ dZ: the oracle forms P = Â X itself
+            X_in = inp.X.astype(np.float64) if l == 0 else h(step.H[l - 1][:n])
+            P = orc.spmm(A, X_in)
+        else:
+            P = h(step.Plp[l][:n]) if bf else h(step.P[l][:n])
         dZin = dZ
         if bf:  # the BF16 GEMMs read bf16 copies of dZ
             dZin = torch.from_numpy(dZ.astype(np.float32)).bfloat16().double().numpy()

@@ -276,6 +276,38 @@ def test_layer_end_to_end_config1(ctx):
     assert rel_err(out["dX"], dX) <= GEMM_TOL
 
 
+@pytest.mark.parametrize("prec", [gsg.GSG_PREC_TF32, gsg.GSG_PREC_BF16])
+def test_layer_chain_order2(ctx, prec):
+    """§7.1 order 2, GSG_ORDER_A_XW: Y = X W, H = ReLU(Â Y); G = Âᵀ dZ, dW = Xᵀ G,
+    dX = (G Wᵀ) ⊙ 1[H_below > 0] -- stage-isolated against the oracle's definitions."""
+    g = graph(6000, 12.0, 1200, 100, 9)
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW_SELF)
+    rng = np.random.default_rng(10)
+    fi, fo = 300, 136
+    X = rng.standard_normal((g.n, fi)).astype(np.float32)
+    W = wl.glorot(rng, fi, fo)
+    dH = rng.standard_normal((g.n, fo)).astype(np.float32)
+    Hb = rng.standard_normal((g.n, fi)).astype(np.float32)
+    sg = ctx.upload(g.indptr, g.indices).normalize()
+    Xd, Wd = dev(X), dev(W)
+    Y, H = empty(g.n, fo), empty(g.n, fo)
+    ctx.layer_forward(sg, Xd, Wd, Y, H, fi, fo, precision=prec, flags=gsg.GSG_ORDER_A_XW)
+    Yg = host(Y)
+    assert rel_err(Yg, orc.gemm(X, W)) <= GEMM_TOL
+    Hg = host(H)
+    assert rel_err(Hg, np.maximum(orc.spmm(A, Yg), 0)) <= SPMM_TOL
+    Xlp = None
+    if prec == gsg.GSG_PREC_BF16:
+        Xlp = torch.zeros((g.n, wl.ld_for(fi, 8)), dtype=torch.bfloat16, device="cuda")[:, :fi]
+        ctx.to_bf16(Xd, Xlp)
+    dW, dX = empty(fi, fo), empty(g.n, fi)
+    ctx.layer_backward(sg, Xd, H, dev(dH), Wd, dW, dX, fi, fo, precision=prec, Plp=Xlp, H_below=dev(Hb),
+                       flags=gsg.GSG_ORDER_A_XW)
+    dZ = orc.relu_mask(dH, Hg)
+    assert rel_err(host(dW), orc.gemm(orc.spmm(A, X), dZ, transA=True)) <= GEMM_TOL
+    assert rel_err(host(dX), np.where(Hb > 0, orc.spmm_t(A, orc.gemm(dZ, W, transB=True)), 0)) <= GEMM_TOL
+
+
 @pytest.mark.parametrize("kind,C", [("softmax", 41), ("sigmoid", 107)])
 def test_head_stage_isolated(ctx, kind, C):
     rng = np.random.default_rng(8)
