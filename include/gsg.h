@@ -234,6 +234,28 @@ GSG_API int gsg_layer_backward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, i
                                const float* d_Hbelow, int64_t ldhb,
                                int precision, int flags);
 
+/* ==== GraphSAGE layer (Eq. 1; backward Eqs. 12-15) ====
+ * The subgraph must be normalized with GSG_NORM_ROW (Ã = D⁻¹ A, no self loop; isolated rows are
+ * zero). Output layout (reading R21, the column slices of Eqs. 12-15 / SPEC S:436): self path in
+ * columns [0, f_half), neighbor path in [f_half, 2 f_half):
+ *   forward:  P = Ã X ;  H = ReLU([X W_s , P W_n])                  (H: n x 2 f_half, ldh)
+ *   backward: dZ = dH ⊙ 1[H > 0] (skipped with GSG_DH_PREMASKED) ;
+ *             dW_s = Xᵀ dZ[:, :f_half] ;  dW_n = Pᵀ dZ[:, f_half:] ;
+ *             dX = (dZ[:, :f_half] W_sᵀ + Ãᵀ (dZ[:, f_half:] W_nᵀ)) ⊙ 1[H_below > 0]
+ * W_s, W_n: f_in x f_half row-major. f_half % 4 == 0 (16-byte column offset of the neighbor
+ * half). TF32 only (GSG_EUNSUPPORTED otherwise). d_dX = NULL skips the input gradient. */
+GSG_API int gsg_sage_forward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, int32_t f_half,
+                             const float* d_X, int64_t ldx, const float* d_Ws, int64_t ldws,
+                             const float* d_Wn, int64_t ldwn, float* d_P, int64_t ldp,
+                             float* d_H, int64_t ldh, int precision, int flags);
+GSG_API int gsg_sage_backward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, int32_t f_half,
+                              const float* d_X, int64_t ldx, const float* d_P, int64_t ldp,
+                              const float* d_H, int64_t ldh, const float* d_dH, int64_t lddh,
+                              const float* d_Ws, int64_t ldws, const float* d_Wn, int64_t ldwn,
+                              float* d_dWs, int64_t lddws, float* d_dWn, int64_t lddwn,
+                              float* d_dX, int64_t lddx, const float* d_Hbelow, int64_t ldhb,
+                              int precision, int flags);
+
 /* ==== classifier head + CE loss (SUPPORT row a8) ======================================= */
 /* S = H_L W_mlp ; S+ = ReLU(S) ; Y = softmax_rows(S+) (GSG_HEAD_SOFTMAX, labels int32[n]
  * class ids) or sigmoid(S+) (GSG_HEAD_SIGMOID, labels uint8[n x C] indicators, ld C);

@@ -168,6 +168,27 @@ def layer_backward(A: AHat, P, Z, dH, W, need_dX: bool = True, premasked: bool =
     return dZ, dW, T, dX
 
 
+def sage_forward(Abar: AHat, X, Ws, Wn):
+    """GraphSAGE layer, Eq. 1 with Ã = D⁻¹A (normalize(..., NORM_ROW)); column layout
+    [self | neighbor] per the slices of Eqs. 12-15 (reading R21). Returns P = ÃX, Z, H."""
+    X = _f64(X)
+    P = spmm(Abar, X)
+    Z = np.hstack([gemm(X, Ws), gemm(P, Wn)])
+    return P, Z, relu(Z)
+
+
+def sage_backward(Abar: AHat, X, P, Z, dH, Ws, Wn, premasked: bool = False):
+    """Eqs. 12-15: dW_s = Xᵀ mask(dH)[:, :f/2], dW_n = (ÃX)ᵀ mask(dH)[:, f/2:],
+    dX = mask(dH)[:, :f/2] W_sᵀ + Ãᵀ mask(dH)[:, f/2:] W_nᵀ."""
+    dZ = _f64(dH) if premasked else relu_mask(dH, Z)
+    fh = np.asarray(Ws).shape[1]
+    dZs, dZn = np.ascontiguousarray(dZ[:, :fh]), np.ascontiguousarray(dZ[:, fh:])
+    dWs = gemm(X, dZs, transA=True)
+    dWn = gemm(P, dZn, transA=True)
+    dX = gemm(dZs, Ws, transB=True) + spmm_t(Abar, gemm(dZn, Wn, transB=True))
+    return dZ, dWs, dWn, dX
+
+
 def head(S, labels, kind: str):
     """Eqs. 2-4 forward + Eqs. 9-10 backward. Returns loss, Y, dS."""
     S = _f64(S)

@@ -63,6 +63,10 @@ _SIGS = {
                                   _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _int]),
     "gsg_head": (_int, [_vp, _i32, _i32, _i32, _int, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
                         _vp, _i64, _vp, _int]),
+    "gsg_sage_forward": (_int, [_vp, _vp, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int,
+                                _int]),
+    "gsg_sage_backward": (_int, [_vp, _vp, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp,
+                                 _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _int]),
     "gsg_nccl_unique_id": (_int, [_vp]),
     "gsg_nccl_comm_init": (_int, [_vp, _int, _int, _vp, ctypes.POINTER(_vp)]),
     "gsg_nccl_comm_destroy": (_int, [_vp]),
@@ -266,6 +270,18 @@ class Context:
                                  _ptr(H) or None, _ld(H), _ptr(dH), _ld(dH), _ptr(dHlp) or None, _ld(dHlp),
                                  _ptr(W), _ld(W), _ptr(dW), _ld(dW), _ptr(dX) or None, _ld(dX), _ptr(dXlp) or None,
                                  _ld(dXlp), _ptr(H_below) or None, _ld(H_below), precision, flags))
+
+    def sage_forward(self, sg: Subgraph, X, Ws, Wn, P, H, f_in: int, f_half: int, precision=GSG_PREC_TF32,
+                     flags: int = 0):
+        check(gsg_sage_forward(self.h, sg.h, f_in, f_half, _ptr(X), _ld(X), _ptr(Ws), _ld(Ws), _ptr(Wn), _ld(Wn),
+                               _ptr(P), _ld(P), _ptr(H), _ld(H), precision, flags))
+
+    def sage_backward(self, sg: Subgraph, X, P, H, dH, Ws, Wn, dWs, dWn, dX, f_in: int, f_half: int, H_below=None,
+                      precision=GSG_PREC_TF32, flags: int = 0):
+        check(gsg_sage_backward(self.h, sg.h, f_in, f_half, _ptr(X), _ld(X), _ptr(P), _ld(P), _ptr(H) or None, _ld(H),
+                                _ptr(dH), _ld(dH), _ptr(Ws), _ld(Ws), _ptr(Wn), _ld(Wn), _ptr(dWs), _ld(dWs),
+                                _ptr(dWn), _ld(dWn), _ptr(dX) or None, _ld(dX), _ptr(H_below) or None, _ld(H_below),
+                                precision, flags))
 
     def head(self, HL, Wm, labels, S, dS, dWm, dHL, n: int, f: int, C: int, kind: int, loss, dHlp=None,
              precision=GSG_PREC_TF32):

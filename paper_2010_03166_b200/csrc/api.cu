@@ -102,6 +102,7 @@ int alloc_subgraph(gsg_ctx* ctx, int32_t n, int64_t nnz, bool has_values, gsg_su
   if (has_values) A((void**)&sg->values, sizeof(float) * nnz);
   A((void**)&sg->rowptr, sizeof(int32_t) * (n + 1));
   A((void**)&sg->perm, sizeof(int32_t) * n);
+  A((void**)&sg->rowval, sizeof(float) * n);
   A((void**)&sg->counters, sizeof(int32_t) * (3 * kBins + 8));
   if (e != cudaSuccess) {
     gsg_subgraph_free(sg);
@@ -283,8 +284,9 @@ GSG_API int gsg_subgraph_assign(gsg_ctx_t c, gsg_subgraph_t sg, int32_t n, int64
   }
   DeviceGuard dg(c->device);
   if (n > sg->cap_n) {
-    cudaFree(sg->indptr); cudaFree(sg->rowptr); cudaFree(sg->perm);
-    sg->indptr = nullptr; sg->rowptr = sg->perm = nullptr;
+    cudaFree(sg->indptr); cudaFree(sg->rowptr); cudaFree(sg->perm); cudaFree(sg->rowval);
+    sg->indptr = nullptr; sg->rowptr = sg->perm = nullptr; sg->rowval = nullptr;
+    GSG_CUDA(cudaMalloc((void**)&sg->rowval, sizeof(float) * (n > 0 ? n : 1)));
     GSG_CUDA(cudaMalloc((void**)&sg->indptr, sizeof(int64_t) * (n + 1)));
     GSG_CUDA(cudaMalloc((void**)&sg->rowptr, sizeof(int32_t) * (n + 1)));
     GSG_CUDA(cudaMalloc((void**)&sg->perm, sizeof(int32_t) * (n > 0 ? n : 1)));
@@ -375,7 +377,7 @@ GSG_API int gsg_subgraph_free(gsg_subgraph_t sg) {
   DeviceGuard dg(sg->device);
   cudaFree(sg->indptr); cudaFree(sg->indices); cudaFree(sg->values);
   cudaFree(sg->rowptr); cudaFree(sg->col); cudaFree(sg->val); cudaFree(sg->valT);
-  cudaFree(sg->perm); cudaFree(sg->counters);
+  cudaFree(sg->perm); cudaFree(sg->rowval); cudaFree(sg->counters);
   delete sg;
   return GSG_OK;
 }
@@ -534,6 +536,69 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   if (rc) return rc;
   // dX = Âᵀ T [⊙ 1[H_below > 0]]   (row a7, fused a4 of the layer below)
   return spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, dXlp, lddxlp, Hbelow, ldhb);
+}
+
+GSG_API int gsg_sage_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32_t fh, const float* X, int64_t ldx,
+                             const float* Ws, int64_t ldws, const float* Wn, int64_t ldwn, float* P, int64_t ldp,
+                             float* H, int64_t ldh, int precision, int flags) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
+  GSG_CHECK(precision == GSG_PREC_TF32, GSG_EUNSUPPORTED, "GraphSAGE layer: TF32 only");
+  GSG_CHECK(f_in >= 1 && fh >= 1 && fh % 4 == 0, GSG_EINVAL, "f_in=%d f_half=%d (f_half %% 4 == 0 required)", f_in, fh);
+  GSG_CHECK(X && Ws && Wn && P && H && ldh >= 2 * fh, GSG_EINVAL, "NULL argument or ldh < 2 f_half");
+  DeviceGuard dg(c->device);
+  const int n = sg->n;
+  const int epi = (flags & GSG_NO_RELU) ? GSG_EPI_NONE : GSG_EPI_RELU;
+  int rc = spmm_launch(c, sg, 0, f_in, X, ldx, P, ldp, nullptr, 0, nullptr, 0);  // P = Ã X
+  if (rc) return rc;
+  rc = gemm_launch(c, n, fh, f_in, X, ldx, 0, Ws, ldws, 0, H, ldh, nullptr, 0, precision, epi, nullptr, 0, 0, 0);
+  if (rc) return rc;
+  return gemm_launch(c, n, fh, f_in, P, ldp, 0, Wn, ldwn, 0, H + fh, ldh, nullptr, 0, precision, epi, nullptr, 0, 0, 0);
+}
+
+GSG_API int gsg_sage_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32_t fh, const float* X, int64_t ldx,
+                              const float* P, int64_t ldp, const float* H, int64_t ldh, const float* dH, int64_t lddh,
+                              const float* Ws, int64_t ldws, const float* Wn, int64_t ldwn, float* dWs, int64_t lddws,
+                              float* dWn, int64_t lddwn, float* dX, int64_t lddx, const float* Hbelow, int64_t ldhb,
+                              int precision, int flags) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
+  GSG_CHECK(precision == GSG_PREC_TF32, GSG_EUNSUPPORTED, "GraphSAGE layer: TF32 only");
+  GSG_CHECK(f_in >= 1 && fh >= 1 && fh % 4 == 0, GSG_EINVAL, "f_in=%d f_half=%d (f_half %% 4 == 0 required)", f_in, fh);
+  GSG_CHECK(X && P && dH && Ws && Wn && dWs && dWn, GSG_EINVAL, "NULL argument");
+  GSG_CHECK((flags & GSG_DH_PREMASKED) || H, GSG_EINVAL, "H is needed unless GSG_DH_PREMASKED");
+  GSG_CHECK(lddh >= 2 * fh && lddh % 4 == 0, GSG_EINVAL, "lddh must be >= 2 f_half and a multiple of 4");
+  DeviceGuard dg(c->device);
+  const int n = sg->n;
+  int rc;
+  const float* dZ = dH;
+  int64_t lddz = lddh;
+  if (!(flags & GSG_DH_PREMASKED)) {
+    lddz = round_up(2 * fh, 4);
+    if ((rc = c->ws_dZ.reserve(sizeof(float) * n * lddz))) return rc;
+    if ((rc = mask_launch(c, n, 2 * fh, dH, lddh, H, ldh, (float*)c->ws_dZ.ptr, lddz, nullptr, 0))) return rc;
+    dZ = (const float*)c->ws_dZ.ptr;
+  }
+  const float* dZs = dZ;        // self half    (Eq. 12 / 14 slice [:, 0:f/2])
+  const float* dZn = dZ + fh;   // neighbor half (Eq. 13 / 15 slice [:, f/2:f])
+  // dW_s = Xᵀ dZ_s ; dW_n = Pᵀ dZ_n   (Eqs. 12-13)
+  rc = gemm_launch(c, f_in, fh, n, X, ldx, 1, dZs, lddz, 0, dWs, lddws, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0,
+                   0, (flags & GSG_ACCUM_DW) ? 1 : 0);
+  if (rc) return rc;
+  rc = gemm_launch(c, f_in, fh, n, P, ldp, 1, dZn, lddz, 0, dWn, lddwn, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0,
+                   0, (flags & GSG_ACCUM_DW) ? 1 : 0);
+  if (rc || !dX) return rc;
+  // dX = dZ_s W_sᵀ + Ãᵀ (dZ_n W_nᵀ), gated by H_below   (Eqs. 14-15)
+  const int64_t ldt = round_up(f_in, 4);
+  if ((rc = c->ws_T.reserve(sizeof(float) * n * ldt))) return rc;
+  float* T = (float*)c->ws_T.ptr;
+  rc = gemm_launch(c, n, f_in, fh, dZn, lddz, 0, Wn, ldwn, 1, T, ldt, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0,
+                   0);
+  if (rc) return rc;
+  rc = gemm_launch(c, n, f_in, fh, dZs, lddz, 0, Ws, ldws, 1, dX, lddx, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0,
+                   0, 0);
+  if (rc) return rc;
+  return spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, nullptr, 0, Hbelow, ldhb, 0, /*accum=*/1);
 }
 
 GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, const float* HL, int64_t ldh,

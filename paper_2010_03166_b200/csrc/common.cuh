@@ -101,6 +101,7 @@ struct gsg_subgraph {
   float* val = nullptr;         // [nnz_hat]
   float* valT = nullptr;        // [nnz_hat]
   int32_t* perm = nullptr;      // [n] rows by descending degree bucket
+  float* rowval = nullptr;      // [n] per-row value of the degree modes (1/(d+1) or 1/d), fp64-rounded
   int32_t* counters = nullptr;  // [kBins + 8]: bucket counts ..., [kBins]=n_heavy, [kBins+1]=max_deg
   size_t cap_hat = 0;
 };
@@ -131,7 +132,8 @@ struct ProfScope {
 // launch wrappers implemented in the .cu files
 int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode);
 int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, const float* X, int64_t ldx,
-                float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, int relu = 0);
+                float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, int relu = 0,
+                int accum = 0);
 int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA,
                 const void* B, int64_t ldb, int transB, float* C, int64_t ldc, void* Clp, int64_t ldclp,
                 int precision, int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate);

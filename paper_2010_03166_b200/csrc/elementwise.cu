@@ -86,12 +86,13 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(int n, int C, int kind, c
   }
 }
 
+// One warp, fixed order: lane l sums partials l, l+32, ... then a fixed xor-tree (deterministic).
 __global__ void k_head_final(int nblocks, int n, const float* __restrict__ partial, float* __restrict__ loss) {
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int b = 0; b < nblocks; b++) t += partial[b];
-    *loss = (float)(t / n);
-  }
+  double t = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += 32) t += partial[b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (threadIdx.x == 0) *loss = (float)(t / n);
 }
 
 }  // namespace

@@ -540,14 +540,21 @@ __global__ void k_splitk_reduce(GemmArgs g) {
     const int c = (int)(i % n4) * 4;
     float x[4] = {0.f, 0.f, 0.f, 0.f};
     const int w = min(4, g.N - c);
-    for (int s = 0; s < g.splits; s++) {
-      const float* p = g.ws + ((int64_t)s * g.mpad + row) * g.ldws + c;
-      if (w == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(p);
-        x[0] += v.x; x[1] += v.y; x[2] += v.z; x[3] += v.w;
-      } else {
-        for (int j = 0; j < w; j++) x[j] += p[j];
-      }
+    // ws rows are padded to ldws (multiple of 8 >= N): float4 loads never leave the row. Loads
+    // are issued 8 at a time (independent), sums applied in split order (deterministic).
+    const float4* p = reinterpret_cast<const float4*>(g.ws + (int64_t)row * g.ldws + c);
+    const int64_t sstride4 = (int64_t)g.mpad * g.ldws / 4;
+    int s = 0;
+    for (; s + 8 <= g.splits; s += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) v[u] = __ldg(p + (s + u) * sstride4);
+#pragma unroll
+      for (int u = 0; u < 8; u++) { x[0] += v[u].x; x[1] += v[u].y; x[2] += v[u].z; x[3] += v[u].w; }
+    }
+    for (; s < g.splits; s++) {
+      const float4 v = __ldg(p + s * sstride4);
+      x[0] += v.x; x[1] += v.y; x[2] += v.z; x[3] += v.w;
     }
     float* dst = g.C + (int64_t)row * g.ldc + c;
     for (int j = 0; j < w; j++) {

@@ -9,8 +9,10 @@ namespace {
 __device__ __forceinline__ int bucket_of(int d) { return d <= 0 ? 0 : 32 - __clz(d); }
 
 // rowptr[i] = indptr[i] + self*i ; histogram of degree buckets ; max degree
-__global__ void k_rowptr(int n, const int64_t* __restrict__ indptr, int self, int32_t* __restrict__ rowptr,
-                         int32_t* __restrict__ counters) {
+// ... and the per-row value of the degree modes, rowval[i] = fp32(1/(d_i+1)) (row-self) or
+// fp32(1/d_i) (row), reused by k_fill for Â_ij and, gathered at column j, for Âᵀ_ij = Â_ji.
+__global__ void k_rowptr(int n, const int64_t* __restrict__ indptr, int self, int mode, int32_t* __restrict__ rowptr,
+                         float* __restrict__ rowval, int32_t* __restrict__ counters) {
   __shared__ int hist[kBins];
   __shared__ int mx;
   if (threadIdx.x < kBins) hist[threadIdx.x] = 0;
@@ -19,9 +21,12 @@ __global__ void k_rowptr(int n, const int64_t* __restrict__ indptr, int self, in
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
     rowptr[i] = (int32_t)(indptr[i] + (self ? i : 0));
     if (i < n) {
-      int d = (int)(indptr[i + 1] - indptr[i]) + self;
+      const int d0 = (int)(indptr[i + 1] - indptr[i]);
+      int d = d0 + self;
       atomicAdd(&hist[bucket_of(d)], 1);
       atomicMax(&mx, d);
+      if (mode == GSG_NORM_ROW_SELF) rowval[i] = (float)(1.0 / ((double)d0 + 1.0));
+      else if (mode == GSG_NORM_ROW) rowval[i] = d0 > 0 ? (float)(1.0 / (double)d0) : 0.f;
     }
   }
   __syncthreads();
@@ -38,15 +43,18 @@ __global__ void k_rowptr(int n, const int64_t* __restrict__ indptr, int self, in
 // val that Alg. 4 produces. GSG_NORM_VALUES needs the search (k_transpose_vals).
 __global__ void k_fill(int n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                        const float* __restrict__ values, int mode, const int32_t* __restrict__ rowptr,
-                       int32_t* __restrict__ col, float* __restrict__ val, float* __restrict__ valT) {
+                       const float* __restrict__ rowval, int32_t* __restrict__ col, float* __restrict__ val,
+                       float* __restrict__ valT) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int self = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_SYM_SELF);
+  const bool by_row = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_ROW);
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
     const int64_t b = indptr[i], e = indptr[i + 1];
     const int d = (int)(e - b);
     const int32_t o = rowptr[i];
     const double di = (double)d;
+    const float vi = by_row ? rowval[i] : 0.f;
     int below = 0;  // neighbors with id < i seen so far
     for (int64_t k0 = b; k0 < e; k0 += 32) {
       const int64_t k = k0 + lane;
@@ -55,21 +63,16 @@ __global__ void k_fill(int n, const int64_t* __restrict__ indptr, const int32_t*
       const unsigned lt = __ballot_sync(0xffffffffu, ok && j < i);
       if (ok) {
         const int pos = (int)(k - b) + (self && j > i ? 1 : 0);
-        double a, at = 0.0;
-        if (mode == GSG_NORM_ROW_SELF) {
-          a = 1.0 / (di + 1.0);
-          at = 1.0 / ((double)(indptr[j + 1] - indptr[j]) + 1.0);
-        } else if (mode == GSG_NORM_SYM_SELF) {
-          a = at = 1.0 / sqrt((di + 1.0) * ((double)(indptr[j + 1] - indptr[j]) + 1.0));
-        } else if (mode == GSG_NORM_ROW) {
-          a = 1.0 / di;
-          at = 1.0 / (double)(indptr[j + 1] - indptr[j]);
-        } else {
-          a = (double)values[k];
-        }
         col[o + pos] = j;
-        val[o + pos] = (float)a;
-        if (mode != GSG_NORM_VALUES) valT[o + pos] = (float)at;
+        if (by_row) {                        // Â_ij = rowval[i], Âᵀ_ij = Â_ji = rowval[j]
+          val[o + pos] = vi;
+          valT[o + pos] = __ldg(rowval + j);
+        } else if (mode == GSG_NORM_SYM_SELF) {
+          const float a = (float)(1.0 / sqrt((di + 1.0) * ((double)(indptr[j + 1] - indptr[j]) + 1.0)));
+          val[o + pos] = valT[o + pos] = a;
+        } else {
+          val[o + pos] = values[k];          // GSG_NORM_VALUES: valT by k_transpose_vals
+        }
       }
       below += __popc(lt);
     }
@@ -122,10 +125,24 @@ __global__ void k_bin_offsets(int32_t* counters) {
 
 __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t* __restrict__ counters,
                               int32_t* __restrict__ perm) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int d = rowptr[i + 1] - rowptr[i];
-    const int pos = atomicAdd(&counters[kBins + 2 + bucket_of(d)], 1);
-    perm[pos] = i;
+  // two-level: shared-memory ranks within the block's slice of rows, then one global atomic per
+  // (block, bucket) to reserve the block's range (the order within a bucket is immaterial)
+  __shared__ int cnt[kBins], base[kBins];
+  for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
+    if (threadIdx.x < kBins) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int i = i0 + threadIdx.x;
+    int b = -1, r = 0;
+    if (i < n) {
+      b = bucket_of(rowptr[i + 1] - rowptr[i]);
+      r = atomicAdd(&cnt[b], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < kBins && cnt[threadIdx.x])
+      base[threadIdx.x] = atomicAdd(&counters[kBins + 2 + threadIdx.x], cnt[threadIdx.x]);
+    __syncthreads();
+    if (b >= 0) perm[base[b] + r] = i;
+    __syncthreads();
   }
 }
 
@@ -156,12 +173,12 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   int grid = (n + 1 + T - 1) / T;
   if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
   if (grid < 1) grid = 1;
-  k_rowptr<<<grid, T, 0, st>>>(n, sg->indptr, self, sg->rowptr, sg->counters);
+  k_rowptr<<<grid, T, 0, st>>>(n, sg->indptr, self, mode, sg->rowptr, sg->rowval, sg->counters);
   if (n > 0) {
     int wgrid = (int)(((int64_t)n * 32 + T - 1) / T);
     if (wgrid > ctx->num_sms * 16) wgrid = ctx->num_sms * 16;
     k_fill<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode, sg->rowptr,
-                                sg->col, sg->val, sg->valT);
+                                sg->rowval, sg->col, sg->val, sg->valT);
     if (mode == GSG_NORM_VALUES) {
       k_transpose_vals<<<wgrid, T, 0, st>>>(n, sg->rowptr, sg->col, sg->val, sg->valT, sg->counters + 3 * kBins + 4);
       count_launch(ctx);

@@ -41,6 +41,7 @@ struct SpmmArgs {
   int64_t ldylp4;
   const float4* __restrict__ mask;
   int relu;                  // epilogue ReLU (chain order 2 forward: H = ReLU(Â (X W)))
+  int accum;                 // epilogue Y = Y + result, before the gate (GraphSAGE dX = self + neighbor terms)
   int64_t ldm4;
   const int32_t* __restrict__ perm;
   const int32_t* __restrict__ n_heavy_ptr;
@@ -168,6 +169,10 @@ __device__ __forceinline__ float4 group_row_sum(const SpmmArgs& a, int b, int e,
 }
 
 __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int c4, float4 acc) {
+  if (a.accum) {
+    const float4 o = a.Y[(int64_t)row * a.ldy4 + c4];
+    acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+  }
   if (a.relu) {
     acc.x = fmaxf(acc.x, 0.f);
     acc.y = fmaxf(acc.y, 0.f);
@@ -320,7 +325,8 @@ int launch_k(gsg_ctx* ctx, K kern, int* occ_cache, const SpmmArgs& a, int64_t wa
 }  // namespace
 
 int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, const float* X, int64_t ldx,
-                float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, int relu) {
+                float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, int relu,
+                int accum) {
   GSG_CHECK(sg->norm_mode >= 0, GSG_EINVAL, "subgraph not normalized (call gsg_subgraph_normalize)");
   GSG_CHECK(f >= 1, GSG_EINVAL, "f must be >= 1 (got %d)", f);
   GSG_CHECK(X && Y, GSG_EINVAL, "X and Y must be non-NULL");
@@ -353,6 +359,7 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   a.ldylp4 = ldylp / 4;
   a.mask = reinterpret_cast<const float4*>(mask);
   a.relu = relu;
+  a.accum = accum;
   a.ldm4 = ldm / 4;
   a.perm = sg->perm;
   a.n_heavy_ptr = sg->counters + kBins;

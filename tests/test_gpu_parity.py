@@ -308,6 +308,48 @@ def test_layer_chain_order2(ctx, prec):
     assert rel_err(host(dX), np.where(Hb > 0, orc.spmm_t(A, orc.gemm(dZ, W, transB=True)), 0)) <= GEMM_TOL
 
 
+@pytest.mark.parametrize("f", [8, 200, 512])
+def test_spmm_weighted_adjacency(ctx, f):
+    """General weighted Â (GSG_NORM_VALUES: GraphSAINT-style aggregator normalization):
+    Âᵀ comes from the binary-search gather form of Alg. 4, not a closed form."""
+    g = graph(5000, 14.0, 1100, 90, 12)
+    vals = wl.random_values(g, 13)
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_VALUES, vals)
+    sg = ctx.upload(g.indptr, g.indices, vals).normalize(gsg.GSG_NORM_VALUES)
+    X = np.random.default_rng(f).standard_normal((g.n, f)).astype(np.float32)
+    Y, Yt = empty(g.n, f), empty(g.n, f)
+    ctx.spmm(sg, dev(X), Y)
+    ctx.spmm(sg, dev(X), Yt, transpose=True)
+    assert rel_err(host(Y), orc.spmm(A, X)) <= SPMM_TOL
+    assert rel_err(host(Yt), orc.spmm_t(A, X)) <= SPMM_TOL
+
+
+@pytest.mark.parametrize("fi,fh", [(52, 16), (300, 128)])
+def test_sage_layer(ctx, fi, fh):
+    """GraphSAGE layer (NEXT #2; Eq. 1, Eqs. 12-15), stage-isolated."""
+    g = graph(6000, 10.0, 1500, 120, 14)
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW)
+    rng = np.random.default_rng(fi)
+    X = rng.standard_normal((g.n, fi)).astype(np.float32)
+    Ws, Wn = wl.glorot(rng, fi, fh), wl.glorot(rng, fi, fh)
+    dH = rng.standard_normal((g.n, 2 * fh)).astype(np.float32)
+    Hb = rng.standard_normal((g.n, fi)).astype(np.float32)
+    sg = ctx.upload(g.indptr, g.indices).normalize(gsg.GSG_NORM_ROW)
+    Xd, Wsd, Wnd = dev(X), dev(Ws), dev(Wn)
+    P, H = empty(g.n, fi), empty(g.n, 2 * fh)
+    ctx.sage_forward(sg, Xd, Wsd, Wnd, P, H, fi, fh)
+    Pg, Hg = host(P), host(H)
+    assert rel_err(Pg, orc.spmm(A, X)) <= SPMM_TOL
+    assert rel_err(Hg, np.maximum(np.hstack([orc.gemm(X, Ws), orc.gemm(Pg, Wn)]), 0)) <= GEMM_TOL
+    dWs, dWn, dX = empty(fi, fh), empty(fi, fh), empty(g.n, fi)
+    ctx.sage_backward(sg, Xd, P, H, dev(dH), Wsd, Wnd, dWs, dWn, dX, fi, fh, H_below=dev(Hb))
+    dZ = orc.relu_mask(dH, Hg)
+    _, rWs, rWn, rX = orc.sage_backward(A, X, Pg, Hg, dZ, Ws, Wn, premasked=True)
+    assert rel_err(host(dWs), rWs) <= GEMM_TOL
+    assert rel_err(host(dWn), rWn) <= GEMM_TOL
+    assert rel_err(host(dX), np.where(Hb > 0, rX, 0)) <= GEMM_TOL
+
+
 @pytest.mark.parametrize("kind,C", [("softmax", 41), ("sigmoid", 107)])
 def test_head_stage_isolated(ctx, kind, C):
     rng = np.random.default_rng(8)

@@ -280,6 +280,46 @@ def test_model_finite_differences(kind, C):
     _fd_check(lambda w: loss_of(Ws, w), Wm, out["dW_mlp"], coords, sign_fun=lambda w: signs(Ws, w))
 
 
+def test_sage_forward_special_cases_and_dense():
+    """GraphSAGE (Eq. 1): an isolated node's neighbor half is 0 (Ã row = 0, SPEC S:120
+    design decision); W_s = W_n = I with X >= 0 gives [X | ÃX]; dense D⁻¹A brute force."""
+    g = rand_graph(50, 4.0, 30)
+    ip = np.concatenate([g.indptr, [g.indptr[-1]]]).astype(np.int64)   # append an isolated node
+    A = orc.normalize(ip, g.indices, orc.NORM_ROW)
+    n = g.n + 1
+    rng = np.random.default_rng(31)
+    Xp = np.abs(rng.standard_normal((n, 6)))
+    _, _, H = orc.sage_forward(A, Xp, np.eye(6), np.eye(6))
+    Ad = dense_adj(wl.CSR(ip, g.indices))
+    d = Ad.sum(1)
+    Abar = np.diag(np.where(d > 0, 1 / np.maximum(d, 1), 0)) @ Ad
+    np.testing.assert_allclose(H, np.hstack([Xp, Abar @ Xp]), atol=1e-14)
+    assert not H[-1, 6:].any()
+    X = rng.standard_normal((n, 6))
+    Ws, Wn = rng.standard_normal((6, 4)), rng.standard_normal((6, 4))
+    _, Z, H = orc.sage_forward(A, X, Ws, Wn)
+    np.testing.assert_allclose(Z, np.hstack([X @ Ws, Abar @ X @ Wn]), rtol=1e-13, atol=1e-13)
+
+
+def test_sage_backward_finite_differences():
+    """Eqs. 12-15 against central differences of <H, dH> w.r.t. W_s, W_n and X."""
+    g = rand_graph(30, 5.0, 32)
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW)
+    rng = np.random.default_rng(33)
+    X = rng.standard_normal((g.n, 5))
+    Ws, Wn = rng.standard_normal((5, 3)), rng.standard_normal((5, 3))
+    dH = rng.standard_normal((g.n, 6))
+    P, Z, H = orc.sage_forward(A, X, Ws, Wn)
+    _, dWs, dWn, dX = orc.sage_backward(A, X, P, Z, dH, Ws, Wn)
+    loss = lambda x, ws, wn: float(np.sum(orc.sage_forward(A, x, ws, wn)[2] * dH))
+    sign = lambda x, ws, wn: orc.sage_forward(A, x, ws, wn)[1] > 0
+    cw = [(i, j) for i in range(5) for j in range(3)]
+    _fd_check(lambda w: loss(X, w, Wn), Ws, dWs, cw, sign_fun=lambda w: sign(X, w, Wn))
+    _fd_check(lambda w: loss(X, Ws, w), Wn, dWn, cw, sign_fun=lambda w: sign(X, Ws, w))
+    cx = [(int(i), int(j)) for i, j in zip(rng.integers(0, g.n, 20), rng.integers(0, 5, 20))]
+    _fd_check(lambda x: loss(x, Ws, Wn), X, dX, cx, sign_fun=lambda x: sign(x, Ws, Wn))
+
+
 def test_head_closed_forms():
     n, C = 8, 41
     loss, Y, dS = orc.head(np.zeros((n, C)), np.zeros(n, np.int32), "softmax")
