@@ -393,6 +393,15 @@ def main():
                 "peak_source": peaks["source"], "launches": sp["launches"], "kernel_ms": sp["ms"],
                 "share_of_step": sp["ms"] / prof_ms if prof_ms > 0 else None,
                 "timing": "per-launch CUDA events on the launch stream, second pass of the same K steps"}
+    l2path = os.path.join(ROOT, "profiles", "r01_l2bw.json")
+    if os.path.exists(l2path):
+        with open(l2path) as f:
+            l2 = json.load(f)
+        ceil = l2.get("l2_gather1k_gbs") or l2.get("l2_gather512_gbs")
+        roofline["l2_gather_ceiling"] = {
+            "gbs": ceil, "frac": spmm_gbs / ceil if ceil else None,
+            "source": "tools/l2bw.cu: random 1 KB row gathers from an L2-resident 82 MB matrix on this pool's B200 "
+                      "(the SpMM's X is L2-resident, so this, not HBM, is its binding ceiling)"}
     gm = prof["gemm"]
     tf32_peak = peaks["bf16_tflops_sustained"] / 2.0  # TF32 = 1/2 of BF16 (nominal ratio), sustained
     gemm_tflops = gm["alg_flops"] / (gm["ms"] / 1e3) / 1e12 if gm["ms"] > 0 else 0.0
