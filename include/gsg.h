@@ -263,12 +263,16 @@ GSG_API int gsg_sage_backward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, in
  * dS = (Y - Ybar)/n ⊙ 1[S > 0] ; dW_mlp = H_Lᵀ dS ; dH_L = (dS W_mlpᵀ) ⊙ 1[H_L > 0]
  * (the returned dH_L is the top GCN layer's dZ, i.e. already premasked).
  *   d_S, d_dS    n x C fp32 scratch/outputs (ld lds); d_loss: one device float.
- *   d_dHlp       optional bf16 copy of dH_L (for BF16 layer backward). */
+ *   d_dHlp       optional bf16 copy of dH_L (for BF16 layer backward).
+ *   d_node_w     optional per-node loss weights λ_i (device float[n]; GraphSAINT loss
+ *                normalization): loss = Σ_i λ_i CE_i and dS_i = λ_i (Y_i - Ybar_i) ⊙
+ *                1[S_i > 0]. NULL = λ_i = 1/n (the mean above). */
 GSG_API int gsg_head(gsg_ctx_t ctx, int32_t n, int32_t f, int32_t C, int kind,
                      const float* d_HL, int64_t ldh, const float* d_Wmlp, int64_t ldw,
                      const void* d_labels, float* d_S, float* d_dS, int64_t lds,
                      float* d_dWmlp, int64_t lddw, float* d_dHL, int64_t lddh,
-                     void* d_dHlp, int64_t lddhlp, float* d_loss, int precision);
+                     void* d_dHlp, int64_t lddhlp, float* d_loss, int precision,
+                     const float* d_node_w);
 
 /* ==== data parallelism (row a9) ======================================================== */
 /* NCCL plumbing (libnccl.so.2 is resolved at run time; the process's already-loaded copy,

@@ -52,7 +52,7 @@ def lib():
         L.oracle_gemm.restype = None
         L.oracle_gemm.argtypes = [i32, i32, i32, vp, i64, cint, vp, i64, cint, vp, i64]
         L.oracle_head.restype = dbl
-        L.oracle_head.argtypes = [i32, i32, vp, i64, cint, vp, vp, vp, vp]
+        L.oracle_head.argtypes = [i32, i32, vp, i64, cint, vp, vp, vp, vp, vp]
         _lib = L
     return _lib
 
@@ -189,7 +189,7 @@ def sage_backward(Abar: AHat, X, P, Z, dH, Ws, Wn, premasked: bool = False):
     return dZ, dWs, dWn, dX
 
 
-def head(S, labels, kind: str):
+def head(S, labels, kind: str, node_w=None):
     """Eqs. 2-4 forward + Eqs. 9-10 backward. Returns loss, Y, dS."""
     S = _f64(S)
     n, C = S.shape
@@ -205,7 +205,8 @@ def head(S, labels, kind: str):
         k = 1
     else:
         raise ValueError(kind)
-    loss = lib().oracle_head(n, C, _p(S), C, k, _p(cls), _p(ind), _p(Y), _p(dS))
+    w = None if node_w is None else _f64(node_w)
+    loss = lib().oracle_head(n, C, _p(S), C, k, _p(cls), _p(ind), None if w is None else _p(w), _p(Y), _p(dS))
     return loss, Y, dS
 
 

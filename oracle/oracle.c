@@ -163,12 +163,16 @@ void oracle_gemm(int32_t M, int32_t N, int32_t K, const double* A, int64_t lda, 
  *   kind 1: L = (1/n) sum_{i,c} [log(1+e^-|s|) + max(s,0) - ybar*s],  s = S+[i,c]
  *                                                                (labels: uint8 indicator)
  *   dS+ = (Y - Ybar)/n ;  dS = dS+ * 1[S > 0]  (mask of the head's ReLU, R4)
+ * With per-node weights w (GraphSAINT loss normalization: "the loss L_s would be
+ * computed with weighted sum"), 1/n is replaced by w[i] in both L and dS+; w = NULL means 1/n.
  * Returns the loss; writes Y and dS (n x C, ld C). */
 double oracle_head(int32_t n, int32_t C, const double* S, int64_t lds, int kind,
-                   const int32_t* cls, const uint8_t* ind, double* Y, double* dS) {
+                   const int32_t* cls, const uint8_t* ind, const double* w, double* Y, double* dS) {
   double loss = 0.0;
 #pragma omp parallel for reduction(+ : loss) schedule(static)
   for (int32_t i = 0; i < n; i++) {
+    const double lam = w ? w[i] : 1.0 / n;
+    double li = 0.0;
     const double* s = S + (int64_t)i * lds;
     double* y = Y + (int64_t)i * C;
     double* g = dS + (int64_t)i * C;
@@ -182,19 +186,20 @@ double oracle_head(int32_t n, int32_t C, const double* S, int64_t lds, int kind,
         double sp = s[c] > 0 ? s[c] : 0.0;
         y[c] = exp(sp - lse);
         double ybar = (c == cls[i]) ? 1.0 : 0.0;
-        g[c] = (s[c] > 0) ? (y[c] - ybar) / n : 0.0;
+        g[c] = (s[c] > 0) ? lam * (y[c] - ybar) : 0.0;
       }
       double spy = s[cls[i]] > 0 ? s[cls[i]] : 0.0;
-      loss += -(spy - lse);
+      li = -(spy - lse);
     } else {
       for (int32_t c = 0; c < C; c++) {
         double sp = s[c] > 0 ? s[c] : 0.0;
         double ybar = ind[(int64_t)i * C + c] ? 1.0 : 0.0;
         y[c] = 1.0 / (1.0 + exp(-sp));
-        loss += log1p(exp(-fabs(sp))) + (sp > 0 ? sp : 0.0) - ybar * sp;
-        g[c] = (s[c] > 0) ? (y[c] - ybar) / n : 0.0;
+        li += log1p(exp(-fabs(sp))) + (sp > 0 ? sp : 0.0) - ybar * sp;
+        g[c] = (s[c] > 0) ? lam * (y[c] - ybar) : 0.0;
       }
     }
+    loss += lam * li;
   }
-  return loss / n;
+  return loss;
 }

@@ -62,7 +62,7 @@ _SIGS = {
     "gsg_layer_backward": (_int, [_vp, _vp, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp,
                                   _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _int]),
     "gsg_head": (_int, [_vp, _i32, _i32, _i32, _int, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
-                        _vp, _i64, _vp, _int]),
+                        _vp, _i64, _vp, _int, _vp]),
     "gsg_sage_forward": (_int, [_vp, _vp, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int,
                                 _int]),
     "gsg_sage_backward": (_int, [_vp, _vp, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp,
@@ -284,10 +284,10 @@ class Context:
                                 precision, flags))
 
     def head(self, HL, Wm, labels, S, dS, dWm, dHL, n: int, f: int, C: int, kind: int, loss, dHlp=None,
-             precision=GSG_PREC_TF32):
+             precision=GSG_PREC_TF32, node_w=None):
         check(gsg_head(self.h, n, f, C, kind, _ptr(HL), _ld(HL), _ptr(Wm), _ld(Wm), _ptr(labels), _ptr(S), _ptr(dS),
                        _ld(S), _ptr(dWm), _ld(dWm), _ptr(dHL), _ld(dHL), _ptr(dHlp) or None, _ld(dHlp), _ptr(loss),
-                       precision))
+                       precision, _ptr(node_w) or None))
 
     # ---- data parallel ----
     @staticmethod

@@ -603,7 +603,8 @@ GSG_API int gsg_sage_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
 
 GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, const float* HL, int64_t ldh,
                      const float* Wm, int64_t ldw, const void* labels, float* S, float* dS, int64_t lds, float* dWm,
-                     int64_t lddw, float* dHL, int64_t lddh, void* dHlp, int64_t lddhlp, float* loss, int precision) {
+                     int64_t lddw, float* dHL, int64_t lddh, void* dHlp, int64_t lddhlp, float* loss, int precision,
+                     const float* node_w) {
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(kind == GSG_HEAD_SOFTMAX || kind == GSG_HEAD_SIGMOID, GSG_EINVAL, "bad head kind %d", kind);
   GSG_CHECK(n >= 1 && f >= 1 && C >= 1, GSG_EINVAL, "bad head sizes n=%d f=%d C=%d", n, f, C);
@@ -613,7 +614,7 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
   DeviceGuard dg(c->device);
   int rc = gemm_launch(c, n, C, f, HL, ldh, 0, Wm, ldw, 0, S, lds, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
   if (rc) return rc;
-  if ((rc = head_loss_launch(c, n, C, kind, S, lds, labels, dS, loss))) return rc;
+  if ((rc = head_loss_launch(c, n, C, kind, S, lds, labels, node_w, dS, loss))) return rc;
   rc = gemm_launch(c, f, C, n, HL, ldh, 1, dS, lds, 0, dWm, lddw, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
   if (rc) return rc;
   return gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, GSG_PREC_TF32, GSG_EPI_MASK, HL, ldh, 0, 0);

@@ -141,5 +141,5 @@ int to_bf16_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t l
 int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh, const float* H, int64_t ldh,
                 float* dZ, int64_t lddz, void* dZlp, int64_t lddzlp);
 int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64_t lds, const void* labels,
-                     float* dS, float* loss);
+                     const float* node_w, float* dS, float* loss);
 }  // namespace gsg

@@ -38,15 +38,16 @@ constexpr int kHeadBlocks = 256;  // fixed grid -> fixed reduction order (determ
 // One warp per row. S+ = ReLU(S); Y = softmax(S+) or sigmoid(S+); per-row CE; dS = (Y-Ybar)/n ⊙ 1[S>0].
 __global__ void __launch_bounds__(kHeadThreads) k_head(int n, int C, int kind, const float* __restrict__ S, int64_t lds,
                                                        const int32_t* __restrict__ cls, const uint8_t* __restrict__ ind,
-                                                       float* __restrict__ dS, float* __restrict__ partial) {
+                                                       const float* __restrict__ node_w, float* __restrict__ dS,
+                                                       float* __restrict__ partial) {
   __shared__ float wsum[kHeadThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = kHeadThreads / 32;
-  const float inv_n = 1.0f / (float)n;
-  float acc = 0.f;  // this lane's share of the block's loss (fixed order)
+  float acc = 0.f;  // this lane's share of the block's (weighted) loss, fixed order
   for (int i = blockIdx.x * nw + warp; i < n; i += gridDim.x * nw) {
     const float* s = S + (int64_t)i * lds;
     float* g = dS + (int64_t)i * lds;
+    const float inv_n = node_w ? node_w[i] : 1.0f / (float)n;  // λ_i (GraphSAINT) or 1/n
     if (kind == GSG_HEAD_SOFTMAX) {
       float mx = 0.f;  // S+ >= 0
       for (int c = lane; c < C; c += 32) mx = fmaxf(mx, fmaxf(s[c], 0.f));
@@ -63,14 +64,14 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(int n, int C, int kind, c
         const float p = expf(fmaxf(sv, 0.f) - lse);
         g[c] = sv > 0.f ? (p - (c == y ? 1.f : 0.f)) * inv_n : 0.f;
       }
-      if (lane == 0) acc += lse - fmaxf(s[y], 0.f);
+      if (lane == 0) acc += inv_n * (lse - fmaxf(s[y], 0.f));
     } else {
       for (int c = lane; c < C; c += 32) {
         const float sv = s[c];
         const float sp = fmaxf(sv, 0.f);
         const float yb = ind[(int64_t)i * C + c] ? 1.f : 0.f;
         const float p = 1.f / (1.f + expf(-sp));
-        acc += log1pf(expf(-sp)) + sp - yb * sp;
+        acc += inv_n * (log1pf(expf(-sp)) + sp - yb * sp);
         g[c] = sv > 0.f ? (p - yb) * inv_n : 0.f;
       }
     }
@@ -92,7 +93,8 @@ __global__ void k_head_final(int nblocks, int n, const float* __restrict__ parti
   for (int b = threadIdx.x; b < nblocks; b += 32) t += partial[b];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  if (threadIdx.x == 0) *loss = (float)(t / n);
+  if (threadIdx.x == 0) *loss = (float)t;
+  (void)n;
 }
 
 }  // namespace
@@ -115,8 +117,8 @@ int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh,
   return GSG_OK;
 }
 
-int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64_t lds, const void* labels, float* dS,
-                     float* loss) {
+int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64_t lds, const void* labels,
+                     const float* node_w, float* dS, float* loss) {
   int rc = ctx->ws_loss.reserve(sizeof(float) * kHeadBlocks);
   if (rc) return rc;
   float* part = (float*)ctx->ws_loss.ptr;
@@ -124,7 +126,7 @@ int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64
   k_head<<<kHeadBlocks, kHeadThreads, 0, ctx->stream>>>(n, C, kind, S, lds,
                                                         kind == GSG_HEAD_SOFTMAX ? (const int32_t*)labels : nullptr,
                                                         kind == GSG_HEAD_SIGMOID ? (const uint8_t*)labels : nullptr,
-                                                        dS, part);
+                                                        node_w, dS, part);
   k_head_final<<<1, 32, 0, ctx->stream>>>(kHeadBlocks, n, part, loss);
   count_launch(ctx, 2);
   GSG_CUDA(cudaGetLastError());

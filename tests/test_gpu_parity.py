@@ -376,6 +376,24 @@ def test_head_stage_isolated(ctx, kind, C):
     assert rel_err(host(dHL), np.where(HL > 0, orc.gemm(dSg, Wm, transB=True), 0)) <= GEMM_TOL
 
 
+def test_head_node_weights(ctx):
+    """GraphSAINT-weighted loss (NEXT #4): loss = Σ λ_i CE_i, dS_i = λ_i (Y_i − Ȳ_i) ⊙ 1[S_i > 0]."""
+    rng = np.random.default_rng(15)
+    n, f, C = 900, 64, 20
+    HL = np.maximum(rng.standard_normal((n, f)), 0).astype(np.float32)
+    Wm = wl.glorot(rng, f, C) * 6
+    labels = (rng.random((n, C)) < 0.1).astype(np.uint8)
+    lam = rng.uniform(0.2, 2.0, n).astype(np.float32) / n
+    S, dWm, dHL = empty(n, C), empty(f, C), empty(n, f)
+    dS = torch.full((n, S.stride(0)), float("nan"), device="cuda")[:, :C]
+    loss = torch.zeros(1, device="cuda")
+    ctx.head(dev(HL), dev(Wm), torch.from_numpy(labels).cuda(), S, dS, dWm, dHL, n, f, C, gsg.GSG_HEAD_SIGMOID, loss,
+             node_w=torch.from_numpy(lam).cuda())
+    l_ref, _, dS_ref = orc.head(host(S), labels, "sigmoid", lam)
+    assert abs(float(host(loss)[0]) - l_ref) <= 1e-5 * abs(l_ref)
+    assert rel_err(host(dS), dS_ref) <= 1e-5
+
+
 def test_allreduce_single_rank(ctx):
     uid = ctx.nccl_unique_id()
     comm = ctx.nccl_comm_init(1, 0, uid)

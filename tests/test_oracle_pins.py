@@ -349,6 +349,23 @@ def test_head_vs_library_formulas():
     np.testing.assert_allclose(dS, (sig - yb) / n * (S > 0), atol=1e-15)
 
 
+def test_head_node_weights():
+    """GraphSAINT loss normalization: weighted sum of per-node CE; λ = 1/n is the mean."""
+    rng = np.random.default_rng(40)
+    n, C = 16, 5
+    S = rng.standard_normal((n, C))
+    y = rng.integers(0, C, n).astype(np.int32)
+    l0, _, g0 = orc.head(S, y, "softmax")
+    l1, _, g1 = orc.head(S, y, "softmax", np.full(n, 1.0 / n))
+    assert abs(l0 - l1) < 1e-15 and np.allclose(g0, g1, rtol=0, atol=1e-17)
+    lam = rng.uniform(0.01, 0.2, n)
+    l2, Y, g2 = orc.head(S, y, "softmax", lam)
+    Sp = np.maximum(S, 0)
+    ce = -(Sp[np.arange(n), y] - logsumexp(Sp, axis=1))
+    assert abs(l2 - np.sum(lam * ce)) < 1e-13
+    np.testing.assert_allclose(g2, lam[:, None] * (Y - np.eye(C)[y]) * (S > 0), atol=1e-16)
+
+
 def test_permutation_equivariance():
     """Relabelling subgraph nodes permutes P, H, dX and leaves dW unchanged."""
     g = rand_graph(40, 6.0, 26)
