@@ -274,6 +274,42 @@ GSG_API int gsg_head(gsg_ctx_t ctx, int32_t n, int32_t f, int32_t C, int kind,
                      void* d_dHlp, int64_t lddhlp, float* d_loss, int precision,
                      const float* d_node_w);
 
+/* ==== GPU-side frontier sampling + induction ======================= *
+ * Alg. 2 under reading R9, on the device, `count` independent samplers at once
+ * (the paper's inter-sampler parallelism):
+ *   FS_0: m distinct nodes drawn uniformly from the parent's non-isolated nodes (rejection of
+ *         repeats); V_s <- FS_0;
+ *   repeat until |V_s| = n (or 1000 n + 10^6 iterations): pick a frontier slot with
+ *         probability deg(u) / sum_FS deg (Alg. 2 line 4; Fenwick tree in shared memory), pick a
+ *         uniform neighbor u' of u (line 5), replace u by u' in FS (line 6), add u' to V_s if new;
+ *   clip |V_s| to a multiple of `clip` by uniformly random removals (§7.2);
+ *   induce G_s on V_s with ascending local ids (Alg. 2 line 9).
+ * Random draws come from a counter-based generator: draw j of iteration i of sampler k is
+ *   r = mix64(seed_k XOR mix64(4 i + j)),  seed_k = seed + k,
+ *   mix64 = splitmix64 finalizer (z += 0x9E3779B97F4A7C15; z ^= z>>30; z *= 0xBF58476D1CE4E5B9;
+ *           z ^= z>>27; z *= 0x94D049BB133111EB; z ^= z>>31),
+ *   uniform integer below N (N < 2^32): ((r >> 32) * N) >> 32;
+ *   j = 3 for FS_0 draws (i counts attempts), 0 for the frontier slot (x below sum_FS deg,
+ *   slot = smallest i with prefix_i > x), 1 for the neighbor index, 2 for clipping removals.
+ * so any implementation of the same rule reproduces the same subgraphs bit for bit.
+ * The parent (symmetric CSR, ascending rows, no self loops) is uploaded once. */
+typedef struct gsg_parent* gsg_parent_t;
+typedef struct gsg_sample* gsg_sample_t;
+GSG_API int gsg_parent_upload(gsg_ctx_t ctx, int64_t N, int64_t nnz, const int64_t* h_indptr,
+                              const int32_t* h_indices, gsg_parent_t* out);
+GSG_API int gsg_parent_free(gsg_parent_t parent);
+/* Sample and induce `count` subgraphs (sampler k uses seed + k). 1 <= m <= n <= N, m <= 16384,
+ * clip >= 1. Synchronizes the context stream once (to size the induced CSR arrays). */
+GSG_API int gsg_frontier_sample(gsg_ctx_t ctx, gsg_parent_t parent, int32_t n, int32_t m,
+                                int32_t clip, uint64_t seed, int32_t count, gsg_sample_t* out);
+/* Device views of subgraph k (valid until gsg_sample_free): n_k nodes, nnz_k entries,
+ * int64 indptr[n_k+1], int32 indices[nnz_k] (local ids), int32 nodes[n_k] (parent ids,
+ * ascending). Pass them to gsg_subgraph_upload_device to train on the sample. */
+GSG_API int gsg_sample_get(gsg_sample_t s, int32_t k, int32_t* n_k, int64_t* nnz_k,
+                           const int64_t** d_indptr, const int32_t** d_indices,
+                           const int32_t** d_nodes);
+GSG_API int gsg_sample_free(gsg_sample_t s);
+
 /* ==== data parallelism (row a9) ======================================================== */
 /* NCCL plumbing (libnccl.so.2 is resolved at run time; the process's already-loaded copy,
  * e.g. torch's, is reused). The 128-byte unique id is produced on one rank and broadcast

@@ -51,6 +51,10 @@ def lib():
         L.oracle_spmm_t_scatter.argtypes = [i32, i32, vp, vp, vp, vp, i64, i32, i32, vp, i64]
         L.oracle_gemm.restype = None
         L.oracle_gemm.argtypes = [i32, i32, i32, vp, i64, cint, vp, i64, cint, vp, i64]
+        L.oracle_frontier_sample.restype = i32
+        L.oracle_frontier_sample.argtypes = [i64, vp, vp, i32, i32, i32, ctypes.c_uint64, vp]
+        L.oracle_induce.restype = i64
+        L.oracle_induce.argtypes = [i64, vp, vp, i32, vp, vp, vp]
         L.oracle_head.restype = dbl
         L.oracle_head.argtypes = [i32, i32, vp, i64, cint, vp, vp, vp, vp, vp]
         _lib = L
@@ -187,6 +191,28 @@ def sage_backward(Abar: AHat, X, P, Z, dH, Ws, Wn, premasked: bool = False):
     dWn = gemm(P, dZn, transA=True)
     dX = gemm(dZs, Ws, transB=True) + spmm_t(Abar, gemm(dZn, Wn, transB=True))
     return dZ, dWs, dWn, dX
+
+
+def frontier_sample(indptr, indices, n: int, m: int, clip: int, seed: int) -> np.ndarray:
+    """Alg. 2 (reading R9) with the counter-based draws of include/gsg.h; returns the
+    ascending node list V_s (parent ids)."""
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(indices, dtype=np.int32)
+    out = np.empty(n, np.int32)
+    nv = lib().oracle_frontier_sample(ip.shape[0] - 1, _p(ip), _p(ix), n, m, clip, seed, _p(out))
+    return out[:nv]
+
+
+def induce(indptr, indices, nodes):
+    """Induced subgraph on an ascending node list (Alg. 2 line 9): (indptr int64, indices int32)."""
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(indices, dtype=np.int32)
+    nd = np.ascontiguousarray(nodes, dtype=np.int32)
+    sp = np.empty(nd.shape[0] + 1, np.int64)
+    nnz = lib().oracle_induce(ip.shape[0] - 1, _p(ip), _p(ix), nd.shape[0], _p(nd), _p(sp), None)
+    si = np.empty(max(nnz, 1), np.int32)
+    lib().oracle_induce(ip.shape[0] - 1, _p(ip), _p(ix), nd.shape[0], _p(nd), _p(sp), _p(si))
+    return sp, si[:nnz]
 
 
 def head(S, labels, kind: str, node_w=None):

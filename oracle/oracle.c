@@ -203,3 +203,104 @@ double oracle_head(int32_t n, int32_t C, const double* S, int64_t lds, int kind,
   }
   return loss;
 }
+
+/* ---------------------------------------------------------------------------------------
+ * Frontier sampling, Alg. 2 under reading R9, plain and serial, with the
+ * counter-based draws specified in include/gsg.h (so the GPU sampler must reproduce it bit for
+ * bit):  r(i, j) = mix64(seed ^ mix64(4 i + j)),  below(r, N) = ((r >> 32) * N) >> 32.
+ * The frontier pop is written as its definition: scan the frontier in slot order and take the
+ * first slot whose cumulative degree exceeds x (x uniform below the total) -- no tree.
+ * Writes the ascending node list (n_out nodes) into nodes_out[n]. Returns n_out.
+ * --------------------------------------------------------------------------------------- */
+static uint64_t or_mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static uint64_t or_rng(uint64_t seed, uint64_t i, uint32_t j) { return or_mix64(seed ^ or_mix64(4 * i + j)); }
+static uint32_t or_below(uint64_t r, uint32_t N) { return (uint32_t)(((r >> 32) * (uint64_t)N) >> 32); }
+static int or_cmp_i32(const void* a, const void* b) {
+  int32_t x = *(const int32_t*)a, y = *(const int32_t*)b;
+  return (x > y) - (x < y);
+}
+
+int32_t oracle_frontier_sample(int64_t N, const int64_t* indptr, const int32_t* indices, int32_t n, int32_t m,
+                               int32_t clip, uint64_t seed, int32_t* nodes_out) {
+  int32_t* noniso = (int32_t*)malloc(sizeof(int32_t) * (size_t)N);
+  int64_t n_noniso = 0;
+  for (int64_t v = 0; v < N; v++)
+    if (indptr[v + 1] > indptr[v]) noniso[n_noniso++] = (int32_t)v;
+  unsigned char* in_vs = (unsigned char*)calloc((size_t)N, 1);
+  int32_t* fs = (int32_t*)malloc(sizeof(int32_t) * (size_t)m);
+  int32_t* vs = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+  /* Alg. 2 line 1 (R9): m distinct non-isolated nodes, uniform; line 2: V_s <- FS */
+  int32_t cnt = 0;
+  for (uint64_t t = 0; cnt < m; t++) {
+    int32_t c = noniso[or_below(or_rng(seed, t, 3), (uint32_t)n_noniso)];
+    if (in_vs[c]) continue;
+    in_vs[c] = 1;
+    fs[cnt] = c;
+    vs[cnt] = c;
+    cnt++;
+  }
+  int32_t nv = m;
+  const uint64_t max_it = 1000ull * (uint64_t)n + 1000000ull;
+  for (uint64_t it = 0; nv < n && it < max_it; it++) {
+    int64_t total = 0;
+    for (int32_t i = 0; i < m; i++) total += indptr[fs[i] + 1] - indptr[fs[i]];
+    /* line 4: select u in FS with probability deg(u) / sum_FS deg */
+    int64_t x = or_below(or_rng(seed, it, 0), (uint32_t)total);
+    int32_t slot = 0;
+    int64_t cum = 0;
+    for (slot = 0; slot < m; slot++) {
+      cum += indptr[fs[slot] + 1] - indptr[fs[slot]];
+      if (cum > x) break;
+    }
+    int32_t u = fs[slot];
+    int64_t du = indptr[u + 1] - indptr[u];
+    /* line 5: u' uniformly among the neighbors of u */
+    int32_t up = indices[indptr[u] + or_below(or_rng(seed, it, 1), (uint32_t)du)];
+    /* line 6: FS <- (FS \ {u}) U {u'} ; R9: u' joins V_s */
+    fs[slot] = up;
+    if (!in_vs[up]) {
+      in_vs[up] = 1;
+      vs[nv++] = up;
+    }
+  }
+  /* clipping: drop uniformly random nodes until |V_s| is a multiple of clip */
+  int32_t keep = nv / clip * clip;
+  for (uint64_t r = 0; nv > keep; r++) {
+    int32_t j = (int32_t)or_below(or_rng(seed, r, 2), (uint32_t)nv);
+    vs[j] = vs[nv - 1];
+    nv--;
+  }
+  qsort(vs, (size_t)nv, sizeof(int32_t), or_cmp_i32);
+  memcpy(nodes_out, vs, sizeof(int32_t) * (size_t)nv);
+  free(noniso); free(in_vs); free(fs); free(vs);
+  return nv;
+}
+
+/* Induced subgraph on an ascending node list (Alg. 2 line 9): local id = position in the list;
+ * row i holds the local ids of the neighbors of nodes[i] that are in the list, in the parent's
+ * (ascending) order. Two calls: indices_out = NULL returns nnz and fills indptr_out. */
+int64_t oracle_induce(int64_t N, const int64_t* indptr, const int32_t* indices, int32_t n, const int32_t* nodes,
+                      int64_t* indptr_out, int32_t* indices_out) {
+  int32_t* local = (int32_t*)malloc(sizeof(int32_t) * (size_t)N);
+  for (int64_t v = 0; v < N; v++) local[v] = -1;
+  for (int32_t i = 0; i < n; i++) local[nodes[i]] = i;
+  indptr_out[0] = 0;
+  for (int32_t i = 0; i < n; i++) {
+    int64_t c = 0;
+    for (int64_t k = indptr[nodes[i]]; k < indptr[nodes[i] + 1]; k++) {
+      int32_t l = local[indices[k]];
+      if (l >= 0) {
+        if (indices_out) indices_out[indptr_out[i] + c] = l;
+        c++;
+      }
+    }
+    indptr_out[i + 1] = indptr_out[i] + c;
+  }
+  free(local);
+  return indptr_out[n];
+}

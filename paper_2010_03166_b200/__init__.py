@@ -67,6 +67,12 @@ _SIGS = {
                                 _int]),
     "gsg_sage_backward": (_int, [_vp, _vp, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp,
                                  _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _int]),
+    "gsg_parent_upload": (_int, [_vp, _i64, _i64, _vp, _vp, ctypes.POINTER(_vp)]),
+    "gsg_parent_free": (_int, [_vp]),
+    "gsg_frontier_sample": (_int, [_vp, _vp, _i32, _i32, _i32, ctypes.c_uint64, _i32, ctypes.POINTER(_vp)]),
+    "gsg_sample_get": (_int, [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_vp),
+                              ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "gsg_sample_free": (_int, [_vp]),
     "gsg_nccl_unique_id": (_int, [_vp]),
     "gsg_nccl_comm_init": (_int, [_vp, _int, _int, _vp, ctypes.POINTER(_vp)]),
     "gsg_nccl_comm_destroy": (_int, [_vp]),
@@ -162,6 +168,79 @@ class Subgraph:
             self.free()
         except Exception:
             pass
+
+
+class ParentGraph:
+    """Device-resident parent graph for GPU frontier sampling (gsg_parent_t)."""
+
+    def __init__(self, ctx: "Context", indptr: np.ndarray, indices: np.ndarray):
+        ip = np.ascontiguousarray(indptr, dtype=np.int64)
+        ix = np.ascontiguousarray(indices, dtype=np.int32)
+        h = _vp()
+        check(gsg_parent_upload(ctx.h, ip.shape[0] - 1, int(ip[-1]), ip.ctypes.data, ix.ctypes.data, ctypes.byref(h)))
+        self.ctx, self.h = ctx, h.value
+
+    def sample(self, n: int, m: int, seed: int, count: int = 1, clip: int = 16) -> "SampleBatch":
+        out = _vp()
+        check(gsg_frontier_sample(self.ctx.h, self.h, n, m, clip, seed, count, ctypes.byref(out)))
+        return SampleBatch(out.value, count)
+
+    def free(self):
+        if self.h:
+            gsg_parent_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class SampleBatch:
+    """`count` GPU-sampled, induced subgraphs (gsg_sample_t)."""
+
+    def __init__(self, handle: int, count: int):
+        self.h, self.count = handle, count
+
+    def get(self, k: int) -> dict:
+        n, nnz, ip, ix, nd = _i32(), _i64(), _vp(), _vp(), _vp()
+        check(gsg_sample_get(self.h, k, ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(ip), ctypes.byref(ix),
+                             ctypes.byref(nd)))
+        return {"n": n.value, "nnz": nnz.value, "d_indptr": ip.value or 0, "d_indices": ix.value or 0,
+                "d_nodes": nd.value or 0}
+
+    def tensors(self, k: int):
+        """Zero-copy torch views of sample k: (indptr int64 [n+1], indices int32 [nnz], nodes int32 [n])."""
+        import torch
+        v = self.get(k)
+        n, nnz = v["n"], v["nnz"]
+        return (torch.as_tensor(_DevView(v["d_indptr"], n + 1, "<i8"), device="cuda"),
+                torch.as_tensor(_DevView(v["d_indices"], nnz, "<i4"), device="cuda"),
+                torch.as_tensor(_DevView(v["d_nodes"], n, "<i4"), device="cuda"))
+
+    def to_host(self, k: int):
+        """Copy sample k back (tests): (indptr int64, indices int32, nodes int32) numpy arrays."""
+        return tuple(t.cpu().numpy() for t in self.tensors(k))
+
+    def free(self):
+        if self.h:
+            gsg_sample_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class _DevView:
+    """__cuda_array_interface__ wrapper of a library-owned device array (no copy)."""
+
+    def __init__(self, ptr: int, count: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr or 0, False),
+                                         "version": 3, "strides": None}
 
 
 class Context:

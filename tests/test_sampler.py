@@ -1,0 +1,131 @@
+"""Frontier sampling + induction (Alg. 2, reading R9).
+
+not-gpu: the oracle sampler/inducer against what Alg. 2 and the definition of an induced
+subgraph fix (budget, distinctness, FS_0 from non-isolated nodes, reachability, degree bias,
+brute-force induction, agreement with the independent workload generator's induction).
+gpu: the device sampler (gsg_frontier_sample) reproduces the oracle bit for bit -- same
+counter-based draws (include/gsg.h) -- and its output trains through the C ABI.
+"""
+import numpy as np
+import pytest
+
+import oracle as orc
+import workload as wl
+
+
+def parent(n=3000, deg=10.0, seed=1):
+    return wl.Parent(n, deg, 2.1, 0.0, seed=seed).csr()
+
+
+def components(csr):
+    lab = -np.ones(csr.n, np.int64)
+    c = 0
+    for s in range(csr.n):
+        if lab[s] >= 0:
+            continue
+        stack = [s]
+        lab[s] = c
+        while stack:
+            v = stack.pop()
+            for w in csr.indices[csr.indptr[v]:csr.indptr[v + 1]]:
+                if lab[w] < 0:
+                    lab[w] = c
+                    stack.append(w)
+        c += 1
+    return lab
+
+
+def test_oracle_sampler_budget_distinct_deterministic():
+    p = parent()
+    v1 = orc.frontier_sample(p.indptr, p.indices, 400, 50, 16, seed=7)
+    v2 = orc.frontier_sample(p.indptr, p.indices, 400, 50, 16, seed=7)
+    v3 = orc.frontier_sample(p.indptr, p.indices, 400, 50, 16, seed=8)
+    assert v1.size == 400 and np.array_equal(v1, v2) and not np.array_equal(v1, v3)
+    assert np.all(np.diff(v1) > 0)                      # ascending, distinct
+    deg = np.diff(p.indptr)
+    assert np.all(deg[v1] > 0)                           # only non-isolated nodes are ever reached
+    clipped = orc.frontier_sample(p.indptr, p.indices, 401, 50, 16, seed=7)
+    assert clipped.size == 400                           # clip to a multiple of 16
+
+
+def test_oracle_sampler_m_equals_n_is_uniform_start():
+    """With m = n no frontier step runs: V_s is FS_0, m distinct non-isolated nodes."""
+    p = parent(500, 6.0, 3)
+    v = orc.frontier_sample(p.indptr, p.indices, 40, 40, 1, seed=11)
+    assert v.size == 40 and len(set(v.tolist())) == 40
+
+
+def test_oracle_sampler_stays_in_start_components():
+    """Every V_s node is reachable from FS_0 (each new node is a neighbor of a frontier node)."""
+    g = wl.CSR(np.array([0, 1, 2, 3, 4, 4], np.int64), np.array([1, 0, 3, 2], np.int32))  # two K2 + isolated
+    v = orc.frontier_sample(g.indptr, g.indices, 2, 1, 1, seed=5)
+    lab = components(g)
+    assert v.size == 2 and lab[v[0]] == lab[v[1]]
+    p = parent(2000, 3.0, 4)  # sparse parent: several components
+    v = orc.frontier_sample(p.indptr, p.indices, 300, 10, 1, seed=6)
+    lab = components(p)
+    assert np.unique(lab[v]).size <= 10
+
+
+def test_oracle_sampler_degree_bias():
+    """Frontier sampling is degree-biased (pops ∝ degree): sampled nodes have a higher
+    mean degree than the parent's non-isolated nodes (statistical pin)."""
+    p = parent(20000, 10.0, 9)
+    deg = np.diff(p.indptr)
+    v = orc.frontier_sample(p.indptr, p.indices, 3000, 300, 1, seed=12)
+    assert deg[v].mean() > 1.5 * deg[deg > 0].mean()
+
+
+def test_oracle_induce_bruteforce_and_independent_impl():
+    p = parent(300, 8.0, 13)
+    v = orc.frontier_sample(p.indptr, p.indices, 80, 20, 1, seed=14)
+    ip, ix = orc.induce(p.indptr, p.indices, v)
+    E = {(int(i), int(j)) for i in range(p.n) for j in p.indices[p.indptr[i]:p.indptr[i + 1]]}
+    expect = [(a, b) for a in range(v.size) for b in range(v.size) if (int(v[a]), int(v[b])) in E]
+    got = [(i, int(j)) for i in range(v.size) for j in ix[ip[i]:ip[i + 1]]]
+    assert got == expect
+    w = wl.Parent.from_csr(p).induce(v.astype(np.int64))  # the generator's own (host C++) induction
+    assert np.array_equal(w.indptr, ip) and np.array_equal(w.indices, ix)
+
+
+# ------------------------------------------------------------------------------ GPU
+@pytest.mark.gpu
+@pytest.mark.parametrize("cid", [1, 2, 5])
+def test_gpu_sampler_matches_oracle(cid):
+    import paper_2010_03166_b200 as gsg
+    cfg = wl.CONFIGS[cid]
+    p = wl.parent_for(cfg).csr()
+    ctx = gsg.Context(0)
+    pg = gsg.ParentGraph(ctx, p.indptr, p.indices)
+    count = 3
+    seed = 1234 + cid
+    batch = pg.sample(cfg.n, cfg.m, seed, count=count, clip=16)
+    for k in range(count):
+        ip, ix, nd = batch.to_host(k)
+        v = orc.frontier_sample(p.indptr, p.indices, cfg.n, cfg.m, 16, seed + k)
+        assert np.array_equal(nd, v), f"sample {k}: node sets differ"
+        rip, rix = orc.induce(p.indptr, p.indices, v)
+        assert np.array_equal(ip, rip) and np.array_equal(ix, rix), f"sample {k}: induced CSR differs"
+    batch.free()
+    pg.free()
+
+
+@pytest.mark.gpu
+def test_gpu_sample_trains():
+    """A GPU-sampled subgraph feeds the layer path directly (device-to-device upload)."""
+    import torch
+    import paper_2010_03166_b200 as gsg
+    cfg = wl.CONFIGS[1]
+    p = wl.parent_for(cfg).csr()
+    ctx = gsg.Context(0)
+    pg = gsg.ParentGraph(ctx, p.indptr, p.indices)
+    batch = pg.sample(cfg.n, cfg.m, 99, count=1)
+    ip, ix, nd = batch.tensors(0)
+    sg = ctx.upload_device(ip, ix).normalize()
+    ipn, ixn = ip.cpu().numpy(), ix.cpu().numpy()
+    A = orc.normalize(ipn, ixn, orc.NORM_ROW_SELF)
+    X = np.random.default_rng(0).standard_normal((sg.n, 56)).astype(np.float32)
+    Y = torch.zeros((sg.n, 56), device="cuda")
+    ctx.spmm(sg, torch.from_numpy(X).cuda(), Y)
+    ref = orc.spmm(A, X)
+    assert np.abs(Y.cpu().numpy() - ref).max() <= 1e-5 * np.abs(ref).max()
