@@ -260,11 +260,11 @@ def main():
 
     nnz_hat = [g.nnz + g.n for g in pool]
 
-    def step(i):
+    def step(i, with_comm=True):
         k = i % len(pool)
         n = pool[k].n
         runner.forward_backward(sgs[k], Xd[k][:n], labels=labd[k], dH_top=None if dHd[k] is None else dHd[k][:n],
-                                comm=comm)
+                                comm=comm if with_comm else None)
         return runner.work_edge_features(nnz_hat[k])
 
     # ---- warm-up (also JITs tensor maps / workspace growth) ----
@@ -283,9 +283,9 @@ def main():
             for k in range(len(pool)):
                 gph = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(gph, stream=stream):
-                    step(k)
+                    step(k, with_comm=False)  # the NCCL all-reduce (a9) is issued eagerly after replay
                 graphs.append(gph)
-            graph_note = "cuda-graph replay of the full step"
+            graph_note = "cuda-graph replay of the step (a1-a8) + eager NCCL all-reduce (a9)"
         except Exception as e:  # noqa: BLE001
             graphs, graph_note = None, f"eager (graph capture failed: {str(e)[:120]})"
             torch.cuda.synchronize()
@@ -296,6 +296,8 @@ def main():
         k = i % len(pool)
         with torch.cuda.stream(stream):
             graphs[k].replay()
+        if comm is not None:
+            ctx.allreduce_grads(comm, [runner.grad_flat], average=True)
         return runner.work_edge_features(nnz_hat[k])
 
     for i in range(2):
