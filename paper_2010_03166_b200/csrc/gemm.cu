@@ -127,6 +127,7 @@ struct GemmArgs {
   int64_t ldws;
   int mpad;         // rows per split in ws (num_m * tile rows): TMA-stored partial tiles never straddle splits
   int tma_store;    // 1: C / ws written by TMA bulk-tensor stores from swizzled smem staging
+  int aux_tma;      // 1: the GSG_EPI_MASK operand is fetched by TMA (tmX) into the staging buffer
   uint32_t idesc;
 };
 
@@ -201,7 +202,7 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
 template <int BN, bool BF16, bool A_MN, bool B_MN, bool CTA2>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
+           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const GemmArgs g) {
   using C = Cfg<BN, BF16, CTA2>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -210,7 +211,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* auxbar = tempty + 2;  // [4] one per epilogue warp: TMA loads of the gate operand
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -226,6 +228,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (g.tma_store) prefetch_tmap(&tmC);
     for (int s = 0; s < C::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CTA2 ? 8 : 4); }
+    for (int w = 0; w < 4; w++) mbar_init(&auxbar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -346,6 +349,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const uint32_t tempty_leader = CTA2 ? map_to_rank(smem_u32(&tempty[0]), 0) : 0u;
     int sbuf = 0;
+    uint32_t aux_phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = group; t < tiles; t += ngroups) {
@@ -364,6 +368,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int col0 = nb * BN + c * 32;
         if (g.tma_store) {
           if (row_base >= g.M || col0 >= g.N) continue;  // warp-uniform: block fully outside C
+          uint8_t* buf = stg + (q * 2 + sbuf) * 4096;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          // ReLU'-gate operand: the 32 x 32 block of aux arrives by TMA into this warp's staging
+          // buffer (coalesced, same swizzle as the store), instead of 32 per-row 128 B reads
+          const bool aux_tma = g.splits == 1 && g.epi == GSG_EPI_MASK && g.aux_tma;
+          if (aux_tma && lane == 0) {
+            mbar_expect_tx(&auxbar[q], 4096);
+            tma_load_2d(buf, &tmX, &auxbar[q], col0, row_base);
+          }
           float x[32];
 #pragma unroll
           for (int i = 0; i < 32; i++) x[i] = __uint_as_float(v[i]);
@@ -371,6 +385,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (g.epi == GSG_EPI_RELU) {
 #pragma unroll
               for (int i = 0; i < 32; i++) x[i] = fmaxf(x[i], 0.f);
+            } else if (aux_tma) {
+              mbar_wait(&auxbar[q], aux_phase);
+              aux_phase ^= 1;
+#pragma unroll
+              for (int j = 0; j < 8; j++) {
+                const float4 m = *reinterpret_cast<const float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
+                x[4 * j] = m.x > 0.f ? x[4 * j] : 0.f;
+                x[4 * j + 1] = m.y > 0.f ? x[4 * j + 1] : 0.f;
+                x[4 * j + 2] = m.z > 0.f ? x[4 * j + 2] : 0.f;
+                x[4 * j + 3] = m.w > 0.f ? x[4 * j + 3] : 0.f;
+              }
             } else if (g.epi == GSG_EPI_MASK && row_ok) {
               const float* ax = g.aux + (int64_t)row * g.ldaux + col0;
               if (col0 + 32 <= g.N) {
@@ -410,8 +435,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
           // stage the 32 x 32 block (128B-swizzled rows) and store it with one TMA bulk-tensor op
-          uint8_t* buf = stg + (q * 2 + sbuf) * 4096;
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; j++)
@@ -643,7 +666,8 @@ int make_store_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols,
 }
 
 template <int BN, bool BF16, bool A_MN, bool B_MN, bool CTA2>
-int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const GemmArgs& g) {
+int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
+             const GemmArgs& g) {
   using C = Cfg<BN, BF16, CTA2>;
   auto kern = k_gemm<BN, BF16, A_MN, B_MN, CTA2>;
   static bool attr_set = false;
@@ -672,18 +696,18 @@ int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const C
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  GSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, g));
+  GSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, g));
   count_launch(ctx);
   return GSG_OK;
 }
 
 template <int BN, bool BF16, bool CTA2>
 int dispatch_major(gsg_ctx* ctx, bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
-                   const CUtensorMap& mc, const GemmArgs& g) {
-  if (!a_mn && !b_mn) return run_gemm<BN, BF16, false, false, CTA2>(ctx, ma, mb, mc, g);
-  if (!a_mn && b_mn) return run_gemm<BN, BF16, false, true, CTA2>(ctx, ma, mb, mc, g);
-  if (a_mn && !b_mn) return run_gemm<BN, BF16, true, false, CTA2>(ctx, ma, mb, mc, g);
-  return run_gemm<BN, BF16, true, true, CTA2>(ctx, ma, mb, mc, g);
+                   const CUtensorMap& mc, const CUtensorMap& mx, const GemmArgs& g) {
+  if (!a_mn && !b_mn) return run_gemm<BN, BF16, false, false, CTA2>(ctx, ma, mb, mc, mx, g);
+  if (!a_mn && b_mn) return run_gemm<BN, BF16, false, true, CTA2>(ctx, ma, mb, mc, mx, g);
+  if (a_mn && !b_mn) return run_gemm<BN, BF16, true, false, CTA2>(ctx, ma, mb, mc, mx, g);
+  return run_gemm<BN, BF16, true, true, CTA2>(ctx, ma, mb, mc, mx, g);
 }
 
 }  // namespace
@@ -746,6 +770,8 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
     int max_s = g.num_kb / 4;                                   // keep >= 4 k-blocks per split
     if (max_s > 64) max_s = 64;
     if (max_s < 1) max_s = 1;
+    if (base_tiles * 2 > units) max_s = 1;  // the grid is already at least half full: no split
+                                            // (measured: the reduction costs more than the tail)
     double best = 1e30;
     splits = 1;
     for (int s = 1; s <= max_s; s++) {
@@ -783,16 +809,23 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   if (g.splits > 1) rc = make_store_map(&mc, g.ws, (int64_t)g.splits * g.mpad, N, g.ldws);
   else rc = make_store_map(&mc, Cp, M, N, ldc);
   if (rc) return rc;
+  // gate operand map (same 32 x 32 swizzled box as the store) for GSG_EPI_MASK
+  CUtensorMap mx = mc;
+  g.aux_tma = 0;
+  if (epilogue == GSG_EPI_MASK && g.tma_store && g.splits == 1) {
+    if ((rc = make_store_map(&mx, aux, M, N, ldaux))) return rc;
+    g.aux_tma = 1;
+  }
   const bool a_mn = transA, b_mn = !transB;
   if (cta2) {
-    rc = bf16 ? dispatch_major<256, true, true>(ctx, a_mn, b_mn, ma, mb, mc, g)
-              : dispatch_major<256, false, true>(ctx, a_mn, b_mn, ma, mb, mc, g);
+    rc = bf16 ? dispatch_major<256, true, true>(ctx, a_mn, b_mn, ma, mb, mc, mx, g)
+              : dispatch_major<256, false, true>(ctx, a_mn, b_mn, ma, mb, mc, mx, g);
   } else if (bf16) {
-    rc = BN == 128 ? dispatch_major<128, true, false>(ctx, a_mn, b_mn, ma, mb, mc, g)
-                   : dispatch_major<256, true, false>(ctx, a_mn, b_mn, ma, mb, mc, g);
+    rc = BN == 128 ? dispatch_major<128, true, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, g)
+                   : dispatch_major<256, true, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, g);
   } else {
-    rc = BN == 128 ? dispatch_major<128, false, false>(ctx, a_mn, b_mn, ma, mb, mc, g)
-                   : dispatch_major<256, false, false>(ctx, a_mn, b_mn, ma, mb, mc, g);
+    rc = BN == 128 ? dispatch_major<128, false, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, g)
+                   : dispatch_major<256, false, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, g);
   }
   if (rc) return rc;
   if (g.splits > 1) {
