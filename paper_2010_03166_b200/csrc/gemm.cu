@@ -24,7 +24,11 @@ namespace gsg {
 namespace {
 
 constexpr int BM = 128;
-constexpr int kGemmThreads = 256;
+// warps 0-3: TMA producer, MMA issuer, TMEM allocator, idle; warps 4-11: epilogue. Two epilogue
+// warps per TMEM lane quarter, each taking half of the tile's columns: the epilogue is bound by
+// its per-warp instruction latency (measured: a K = 64 GEMM spends 2/3 of its time there).
+constexpr int kEpiWarps = 8;
+constexpr int kGemmThreads = 128 + 32 * kEpiWarps;
 
 // ------------------------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -145,10 +149,15 @@ struct Cfg {
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = BNC * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = STAGE_BYTES >= 48 * 1024 ? 4 : 6;
+  static constexpr int STG = 1;                     // staging buffers per epilogue warp
+  // as many operand stages as fit next to the staging buffers (cap 8)
+  static constexpr int STAGES_FIT = (232448 - 1280 - kEpiWarps * STG * 4096) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
-  static constexpr int STG_BYTES = 4 * 2 * 4096;     // 4 epilogue warps x 2 buffers x (32 x 32 fp32)
+  static constexpr int STG_BYTES = kEpiWarps * STG * 4096;  // per epilogue warp: STG x (32 x 32 fp32)
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 256 /*barriers*/;
+  static_assert(SMEM <= 232448, "GEMM smem over the 227 KB per-CTA limit");
+  static_assert(STAGES * 16 + 4 * 8 + kEpiWarps * 8 + 4 <= 256, "GEMM barriers overflow their 256 B");
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -164,8 +173,11 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t ran
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Arrive on the pair leader's barrier. Default (.release.cta) semantics: only the TMEM reads must
+// be ordered before it, and tcgen05.fence::before_thread_sync does that. An explicit .release.cluster
+// compiles to MEMBAR.ALL.GPU + ERRBAR, which drains this thread's outstanding TMA stores every tile.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load whose completion is counted on the pair leader's mbarrier (cta_group::2)
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0, int c1) {
@@ -211,8 +223,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* auxbar = tempty + 2;  // [4] one per epilogue warp: TMA loads of the gate operand
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + 4);
+  uint64_t* auxbar = tempty + 2;  // [kEpiWarps] one per epilogue warp: TMA loads of the gate operand
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -227,8 +239,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     prefetch_tmap(&tmB);
     if (g.tma_store) prefetch_tmap(&tmC);
     for (int s = 0; s < C::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CTA2 ? 8 : 4); }
-    for (int w = 0; w < 4; w++) mbar_init(&auxbar[w], 1);
+    for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CTA2 ? 2 * kEpiWarps : kEpiWarps); }
+    for (int w = 0; w < kEpiWarps; w++) mbar_init(&auxbar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -346,7 +358,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== epilogue (own 128 rows of the tile) =====================
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int q = warp & 3;           // TMEM lane quarter this warp may access
+    const int e = warp - 4;           // epilogue warp index: staging buffers, aux barrier
+    constexpr int CPW = BN / 32 / (kEpiWarps / 4);  // 32-column chunks per warp
+    const int c_begin = (e >> 2) * CPW;
     const uint32_t tempty_leader = CTA2 ? map_to_rank(smem_u32(&tempty[0]), 0) : 0u;
     int sbuf = 0;
     uint32_t aux_phase = 0;
@@ -361,22 +376,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row_base = mb * C::BMT + (int)rank * BM + q * 32;
       const int row = row_base + lane;
       const bool row_ok = row < g.M;
-      for (int c = 0; c < BN / 32; c++) {
+      for (int c = c_begin; c < c_begin + CPW; c++) {
         uint32_t v[32];
         __syncwarp();
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
         const int col0 = nb * BN + c * 32;
         if (g.tma_store) {
           if (row_base >= g.M || col0 >= g.N) continue;  // warp-uniform: block fully outside C
-          uint8_t* buf = stg + (q * 2 + sbuf) * 4096;
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          uint8_t* buf = stg + (e * C::STG + sbuf) * 4096;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::STG - 1) : "memory");
           __syncwarp();
           // ReLU'-gate operand: the 32 x 32 block of aux arrives by TMA into this warp's staging
           // buffer (coalesced, same swizzle as the store), instead of 32 per-row 128 B reads
           const bool aux_tma = g.splits == 1 && g.epi == GSG_EPI_MASK && g.aux_tma;
           if (aux_tma && lane == 0) {
-            mbar_expect_tx(&auxbar[q], 4096);
-            tma_load_2d(buf, &tmX, &auxbar[q], col0, row_base);
+            mbar_expect_tx(&auxbar[e], 4096);
+            tma_load_2d(buf, &tmX, &auxbar[e], col0, row_base);
           }
           float x[32];
 #pragma unroll
@@ -386,7 +401,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
               for (int i = 0; i < 32; i++) x[i] = fmaxf(x[i], 0.f);
             } else if (aux_tma) {
-              mbar_wait(&auxbar[q], aux_phase);
+              mbar_wait(&auxbar[e], aux_phase);
               aux_phase ^= 1;
 #pragma unroll
               for (int j = 0; j < 8; j++) {
@@ -450,7 +465,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                          : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          sbuf ^= 1;
+          if (++sbuf == C::STG) sbuf = 0;
           continue;
         }
         if (!row_ok || col0 >= g.N) continue;
@@ -751,7 +766,8 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   int rc = get_encode();
   if (rc) return rc;
   const int BN = N <= 128 ? 128 : 256;
-  // pair (cta_group::2, 256-row tiles) whenever the shape fills the pair tile; GSG_GEMM_1CTA=1 forces 1-CTA
+  // pair (cta_group::2, 256-row tiles) whenever the shape fills the pair tile; GSG_GEMM_1CTA=1 forces 1-CTA.
+  // (128-wide pair tiles would cut the last-wave waste on 20000 x 1024 but measured 1.35x slower.)
   static const bool force1 = getenv("GSG_GEMM_1CTA") && atoi(getenv("GSG_GEMM_1CTA")) == 1;
   const bool cta2 = !force1 && BN == 256 && M > BM;
   const int BMT = cta2 ? 2 * BM : BM;
