@@ -206,6 +206,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="B independent subgraphs per step as one block-diagonal graph (SURVEY §8(d) batched variant)")
+    ap.add_argument("--flush-l2", action="store_true",
+                    help="flush L2 (write a 2x-L2 buffer) before every step of the per-step timing pass")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = wl.CONFIGS[args.config]
@@ -227,7 +231,10 @@ def main():
     t_setup = time.time()
 
     # ---- host inputs (seeded; outside every timed region) ----
-    pool = [wl.sample_subgraph(cfg, k, rank) for k in range(args.pool)]
+    if args.batch > 1:
+        pool = [wl.sample_batch(cfg, args.batch, k, rank) for k in range(args.pool)]
+    else:
+        pool = [wl.sample_subgraph(cfg, k, rank) for k in range(args.pool)]
     inputs = [wl.make_inputs(cfg, g.n, k, rank) for k, g in enumerate(pool)]
     n_max = max(g.n for g in pool)
 
@@ -259,6 +266,12 @@ def main():
         comm = ctx.nccl_comm_init(world, rank, uid)
 
     nnz_hat = [g.nnz + g.n for g in pool]
+    act_bytes = 4 * n_max * sum(cfg.dims) * 4  # X/P/H/dX-class buffers per step, lower bound
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    l2_note = (f"step working set (>= {act_bytes / 1e6:.0f} MB of activations) exceeds the {l2_bytes / 1e6:.0f} MB L2; "
+               f"{len(pool)} subgraphs rotate" if act_bytes > l2_bytes else
+               f"step working set ({act_bytes / 1e6:.0f} MB) fits the {l2_bytes / 1e6:.0f} MB L2: warm-cache numbers; "
+               "step_ms_dist with --flush-l2 gives the flushed figure")
 
     def step(i, with_comm=True):
         k = i % len(pool)
@@ -322,6 +335,28 @@ def main():
     torch.cuda.synchronize()
     max_ms, total_work = dp.reduce_timing(ms, float(work), device=dev)
     value = total_work / (max_ms / 1e3)
+
+    # ---- per-step distribution: an event pair around every step (optionally after an L2 flush,
+    # outside the bracket) -> p10 / p50 / p90 ms per step ----
+    flush = None
+    if args.flush_l2:
+        l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+        flush = torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        if flush is not None:
+            with torch.cuda.stream(stream):
+                flush.fill_(float(i))
+        evs[i][0].record(stream)
+        step_run(i)
+        evs[i][1].record(stream)
+    stream.synchronize()
+    per_step = sorted(a.elapsed_time(b) for a, b in evs)
+
+    def pct(q):
+        return per_step[min(len(per_step) - 1, int(round(q * (len(per_step) - 1))))]
+    step_dist = {"p10": pct(0.1), "p50": pct(0.5), "p90": pct(0.9),
+                 "l2": "flushed before every step" if flush is not None else "not flushed (working set vs L2 as in config.l2)"}
 
     # ---- the same K steps again with CUDA events around every launch (kernel-level rooflines) ----
     pv0, pv1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -460,14 +495,17 @@ def main():
                "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (SpMM) + tf32 (GEMM)" if cfg.precision == "tf32"
                else "f32 (SpMM) + bf16 (GEMM)", "data": "synthetic",
-               "config": {"workload": f"config{cfg.cid}:{cfg.name}", "nodes_per_gpu": cfg.n,
+               "config": {"workload": f"config{cfg.cid}:{cfg.name}" + (f" x{args.batch} block-diagonal batch"
+                                                                         if args.batch > 1 else ""),
+                          "nodes_per_gpu": max(g.n for g in pool), "subgraphs_per_step": args.batch,
                           "nnz_hat_per_gpu": nnz_hat, "dims": cfg.dims, "head": f"{cfg.head}{cfg.classes}",
                           "parent": {"n": cfg.parent_n, "mean_deg": cfg.parent_mean_deg, "gamma": cfg.gamma},
                           "pool_per_gpu": len(pool), "parallelism": f"dp{world}",
-                          "l2": "step working set (~1 GB of activations) far exceeds the 126 MB L2; subgraphs rotate"},
+                          "l2": l2_note},
                "roofline": roofline, "gemm": gemm_info, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches, "launch_mode": graph_note, "clocks": clk.summary(),
                "stages_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
+               "step_ms_dist": step_dist,
                "setup_s": time.time() - t_setup}
         print(json.dumps(out), flush=True)
     if comm is not None:

@@ -34,52 +34,77 @@ __global__ void k_rowptr(int n, const int64_t* __restrict__ indptr, int self, in
   if (threadIdx.x == 0) atomicMax(&counters[kBins + 1], mx);
 }
 
-// One warp per row: copy the neighbor list inserting the self loop at its sorted position and
-// compute the values of the requested normalization in fp64 (rounded once to fp32).
+// Edge-parallel fill: every raw entry k is placed at its slot of Â, shifted by one past the
+// row's self loop, and given the values of the requested normalization in fp64 (rounded once to
+// fp32). Each thread takes kFillPer entries strided by the grid's thread count (coalesced) and
+// finds each entry's row by a binary search of indptr (20K-row indptr is L1/L2-resident), so no
+// row's length serializes the kernel (a warp-per-row loop spent ~45 us on the 1.3K-degree hubs
+// of config 5). The self loops are written by k_fill_self.
 //
 // For the degree-based modes the transposed value is a closed form of the column's degree
 // (Âᵀ_ij = Â_ji: 1/(d_j+1) row-self, 1/d_j row, val itself for the symmetric mode), written
 // here in the same fp64 -> fp32 rounding as Â_ji, so valT is bit-for-bit the permutation of
 // val that Alg. 4 produces. GSG_NORM_VALUES needs the search (k_transpose_vals).
-__global__ void k_fill(int n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+constexpr int kFillPer = 4;
+__device__ __forceinline__ int row_of(const int64_t* __restrict__ indptr, int n, int64_t k) {
+  int lo = 0, hi = n - 1;  // largest i with indptr[i] <= k (k < nnz, so a non-empty row)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(indptr + mid) <= k) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+__global__ void k_fill(int n, int64_t nnz, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                        const float* __restrict__ values, int mode, const int32_t* __restrict__ rowptr,
                        const float* __restrict__ rowval, int32_t* __restrict__ col, float* __restrict__ val,
                        float* __restrict__ valT) {
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
   const int self = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_SYM_SELF);
   const bool by_row = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_ROW);
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
-    const int64_t b = indptr[i], e = indptr[i + 1];
-    const int d = (int)(e - b);
-    const int32_t o = rowptr[i];
-    const double di = (double)d;
-    const float vi = by_row ? rowval[i] : 0.f;
-    int below = 0;  // neighbors with id < i seen so far
-    for (int64_t k0 = b; k0 < e; k0 += 32) {
-      const int64_t k = k0 + lane;
-      const bool ok = k < e;
-      const int j = ok ? indices[k] : 0x7fffffff;
-      const unsigned lt = __ballot_sync(0xffffffffu, ok && j < i);
-      if (ok) {
-        const int pos = (int)(k - b) + (self && j > i ? 1 : 0);
-        col[o + pos] = j;
-        if (by_row) {                        // Â_ij = rowval[i], Âᵀ_ij = Â_ji = rowval[j]
-          val[o + pos] = vi;
-          valT[o + pos] = __ldg(rowval + j);
-        } else if (mode == GSG_NORM_SYM_SELF) {
-          const float a = (float)(1.0 / sqrt((di + 1.0) * ((double)(indptr[j + 1] - indptr[j]) + 1.0)));
-          val[o + pos] = valT[o + pos] = a;
-        } else {
-          val[o + pos] = values[k];          // GSG_NORM_VALUES: valT by k_transpose_vals
-        }
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < nnz; k0 += T * kFillPer) {
+    int i[kFillPer], j[kFillPer];
+#pragma unroll
+    for (int u = 0; u < kFillPer; u++) {
+      const int64_t k = k0 + u * T;
+      i[u] = k < nnz ? row_of(indptr, n, k) : 0;
+      j[u] = k < nnz ? __ldg(indices + k) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kFillPer; u++) {
+      const int64_t k = k0 + u * T;
+      if (k >= nnz) break;
+      const int r = i[u], c = j[u];
+      const int64_t pos = (int64_t)rowptr[r] + (k - __ldg(indptr + r)) + (self && c > r ? 1 : 0);
+      col[pos] = c;
+      if (by_row) {                          // Â_rc = rowval[r], Âᵀ_rc = Â_cr = rowval[c]
+        val[pos] = __ldg(rowval + r);
+        valT[pos] = __ldg(rowval + c);
+      } else if (mode == GSG_NORM_SYM_SELF) {
+        const double dr = (double)(__ldg(indptr + r + 1) - __ldg(indptr + r));
+        const double dc = (double)(__ldg(indptr + c + 1) - __ldg(indptr + c));
+        val[pos] = valT[pos] = (float)(1.0 / sqrt((dr + 1.0) * (dc + 1.0)));
+      } else {
+        val[pos] = values[k];                // GSG_NORM_VALUES: valT by k_transpose_vals
       }
-      below += __popc(lt);
     }
-    if (self && lane == 0) {
-      col[o + below] = i;
-      val[o + below] = valT[o + below] = (float)(1.0 / (di + 1.0));
+  }
+}
+
+// Self loops (self modes): row i's loop goes after its neighbors with id < i, found by a binary
+// search of the ascending list; value 1/(d_i+1) (row-self: Â_ii; sym: 1/sqrt((d_i+1)^2)).
+__global__ void k_fill_self(int n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                            const int32_t* __restrict__ rowptr, int32_t* __restrict__ col, float* __restrict__ val,
+                            float* __restrict__ valT) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int64_t b = indptr[i], e = indptr[i + 1];
+    int64_t lo = b, hi = e;  // first position with indices[pos] > i
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(indices + mid) < i) lo = mid + 1; else hi = mid;
     }
+    const int32_t pos = rowptr[i] + (int32_t)(lo - b);
+    col[pos] = i;
+    val[pos] = valT[pos] = (float)(1.0 / ((double)(e - b) + 1.0));
   }
 }
 
@@ -177,15 +202,24 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   if (n > 0) {
     int wgrid = (int)(((int64_t)n * 32 + T - 1) / T);
     if (wgrid > ctx->num_sms * 16) wgrid = ctx->num_sms * 16;
-    k_fill<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode, sg->rowptr,
-                                sg->rowval, sg->col, sg->val, sg->valT);
+    if (sg->nnz > 0) {
+      int64_t eg = (sg->nnz + (int64_t)T * kFillPer - 1) / ((int64_t)T * kFillPer);
+      if (eg > (int64_t)ctx->num_sms * 8) eg = (int64_t)ctx->num_sms * 8;
+      k_fill<<<(int)eg, T, 0, st>>>(n, sg->nnz, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode,
+                                    sg->rowptr, sg->rowval, sg->col, sg->val, sg->valT);
+      count_launch(ctx);
+    }
+    if (self) {
+      k_fill_self<<<grid, T, 0, st>>>(n, sg->indptr, sg->indices, sg->rowptr, sg->col, sg->val, sg->valT);
+      count_launch(ctx);
+    }
     if (mode == GSG_NORM_VALUES) {
       k_transpose_vals<<<wgrid, T, 0, st>>>(n, sg->rowptr, sg->col, sg->val, sg->valT, sg->counters + 3 * kBins + 4);
       count_launch(ctx);
     }
     k_bin_offsets<<<1, 32, 0, st>>>(sg->counters);
     k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm);
-    count_launch(ctx, 4);
+    count_launch(ctx, 3);
   } else {
     count_launch(ctx, 1);
   }

@@ -101,3 +101,24 @@ def test_config_shapes(cid):
     st = s.stats()
     if cid == 2:  # SURVEY Appendix A calibration: stated ~200K nnz (±15%)
         assert 170_000 <= st["nnz"] <= 230_000
+
+
+def test_block_diag_batch_structure():
+    """block_diag: disjoint union (config-1 batched variant): sizes add up, every
+    part keeps its own edges (shifted), no edge crosses parts, symmetry is preserved."""
+    cfg = wl.tiny_config(n_parent=300, mean_deg=6.0, n=40, m=8)
+    parts = [wl.sample_subgraph(cfg, k) for k in range(3)]
+    g = wl.block_diag(parts)
+    assert g.n == sum(p.n for p in parts) and g.nnz == sum(p.nnz for p in parts)
+    off = 0
+    for p in parts:
+        for i in range(p.n):
+            row = g.indices[g.indptr[off + i]:g.indptr[off + i + 1]]
+            assert np.array_equal(row, p.indices[p.indptr[i]:p.indptr[i + 1]] + off)
+        off += p.n
+    A = np.zeros((g.n, g.n), np.int8)
+    for i in range(g.n):
+        A[i, g.indices[g.indptr[i]:g.indptr[i + 1]]] = 1
+    assert np.array_equal(A, A.T)
+    b = wl.sample_batch(cfg, 3)
+    assert np.array_equal(b.indptr, g.indptr) and np.array_equal(b.indices, g.indices)

@@ -224,6 +224,30 @@ def sample_subgraph(cfg: Config, k: int = 0, r: int = 0) -> CSR:
     return parent_for(cfg).frontier_sample(cfg.n, cfg.m, cfg.seed(10, k, r))
 
 
+def block_diag(parts: list) -> CSR:
+    """Disjoint union of subgraphs as one CSR (block-diagonal adjacency; node ids of part b are
+    offset by the sizes of parts 0..b-1). The paper trains on independent subgraphs with no
+    dependency between them; batching B of them per launch with a shared W is the
+    same computation as B separate layers, so a small config can fill the GPU (SURVEY §8(d),
+    config 1 "batched variant"). Pure structure: no method arithmetic."""
+    n_off, e_off = 0, 0
+    ips, ixs = [np.zeros(1, np.int64)], []
+    for c in parts:
+        ips.append(c.indptr[1:].astype(np.int64) + e_off)
+        ixs.append(c.indices.astype(np.int64) + n_off)
+        n_off += c.n
+        e_off += c.nnz
+    ix = np.concatenate(ixs) if ixs else np.zeros(0, np.int64)
+    if n_off >= 2**31:
+        raise ValueError("batched subgraph exceeds int32 node ids")
+    return CSR(np.concatenate(ips), ix.astype(np.int32))
+
+
+def sample_batch(cfg: Config, batch: int, slot: int = 0, r: int = 0) -> CSR:
+    """B independent subgraphs (pool indices slot*B .. slot*B+B-1) as one block-diagonal CSR."""
+    return block_diag([sample_subgraph(cfg, slot * batch + b, r) for b in range(batch)])
+
+
 @dataclass
 class Inputs:
     """Dense seeded inputs for one subgraph (unpadded, row-major float32)."""
