@@ -147,6 +147,27 @@ def test_spmm_heavy_rows_and_mask(ctx):
         assert np.array_equal(yl, torch.from_numpy(host(Y).astype(np.float32)).bfloat16().float().numpy())
 
 
+@pytest.mark.parametrize("f", [65, 200, 300, 1024, 1100])
+def test_spmm_dense_frontier(ctx, f):
+    """Dense frontier subgraph (config-5-like density, heavy rows, many shared high-degree
+    neighbors) at widths with full and ragged column chunks (f = 1100: 5 chunks of 55 float4)."""
+    g = graph(20000, 40.0, 2500, 300, 11)
+    d = np.diff(g.indptr) + 1
+    assert (d >= 16).sum() > 300 and d.max() >= 256
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW_SELF)
+    sg = ctx.upload(g.indptr, g.indices).normalize(gsg.GSG_NORM_ROW_SELF)
+    rng = np.random.default_rng(100 + f)
+    X = rng.standard_normal((g.n, f)).astype(np.float32)
+    Y, Yt = empty(g.n, f), empty(g.n, f)
+    ctx.spmm(sg, dev(X), Y)
+    ctx.spmm(sg, dev(X), Yt, transpose=True)
+    assert rel_err(host(Y), orc.spmm(A, X)) <= SPMM_TOL
+    assert rel_err(host(Yt), orc.spmm_t(A, X)) <= SPMM_TOL
+    Y2 = empty(g.n, f)
+    ctx.spmm(sg, dev(X), Y2)
+    assert torch.equal(Y, Y2)
+
+
 def test_spmm_deterministic_and_identity(ctx):
     g = graph(5000, 20.0, 1500, 100, 5)
     sg = ctx.upload(g.indptr, g.indices).normalize()
