@@ -266,6 +266,7 @@ def main():
         comm = ctx.nccl_comm_init(world, rank, uid)
 
     nnz_hat = [g.nnz + g.n for g in pool]
+    nnz_raw = [g.nnz for g in pool]
     act_bytes = 4 * n_max * sum(cfg.dims) * 4  # X/P/H/dX-class buffers per step, lower bound
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     l2_note = (f"step working set (>= {act_bytes / 1e6:.0f} MB of activations) exceeds the {l2_bytes / 1e6:.0f} MB L2; "
@@ -341,6 +342,11 @@ def main():
     torch.cuda.synchronize()
     max_ms, total_work = dp.reduce_timing(ms, float(work), device=dev)
     value = total_work / (max_ms / 1e3)
+    # the same timed steps counted without self loops (nnz instead of nnz'), and in subgraphs/s
+    work_noself = sum(runner.work_edge_features(nnz_raw[i % len(pool)]) for i in range(args.steps))
+    _, total_noself = dp.reduce_timing(ms, float(work_noself), device=dev)
+    value_noself = total_noself / (max_ms / 1e3)
+    subgraphs_per_s = world * args.steps * args.batch / (max_ms / 1e3)
 
     # ---- per-step distribution: an event pair around every step (optionally after an L2 flush,
     # outside the bracket) -> p10 / p50 / p90 ms per step ----
@@ -486,6 +492,21 @@ def main():
                  "kernel_ms": gm["ms"], "launches": gm["launches"],
                  "share_of_step": gm["ms"] / prof_ms if prof_ms > 0 else None}
     gemm_info["frac"] = gemm_tflops / gemm_info["peak"]
+    # Layer-level roofline fraction: ideal step time from the algorithmic totals --
+    # SpMM effective bytes at a memory ceiling + GEMM flops at the tensor peak + the other
+    # kernels' bytes at HBM -- over the measured step time. Against HBM (the contract's number,
+    # > 1 because X is L2-resident) and against the measured L2 random-gather ceiling.
+    step_ms = max_ms / args.steps
+    other_bytes = (prof["normalize"]["alg_bytes"] + prof["other"]["alg_bytes"]) / args.steps
+    gemm_ideal_ms = gm["alg_flops"] / args.steps / (gemm_info["peak"] * 1e12) * 1e3
+    other_ideal_ms = other_bytes / (peaks["hbm_gbs"] * 1e9) * 1e3
+    sp_bytes = sp["alg_bytes"] / args.steps
+    layer_roof = {"hbm": (sp_bytes / (peaks["hbm_gbs"] * 1e9) * 1e3 + gemm_ideal_ms + other_ideal_ms) / step_ms}
+    if "l2_gather_ceiling" in roofline and roofline["l2_gather_ceiling"]["gbs"]:
+        l2g = roofline["l2_gather_ceiling"]["gbs"]
+        layer_roof["l2_gather"] = (sp_bytes / (l2g * 1e9) * 1e3 + gemm_ideal_ms + other_ideal_ms) / step_ms
+    layer_roof["note"] = ("(SpMM effective bytes / memory ceiling + GEMM flops / tensor peak + other bytes / HBM) "
+                          "/ measured step time")
 
     # ---- CPU baseline: the oracle on host cores (rank 0, N = 1 only) ----
     cpu = None
@@ -512,6 +533,8 @@ def main():
                "gpu_launches": launches, "launch_mode": graph_note, "clocks": clk.summary(),
                "stages_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
                "step_ms_dist": step_dist,
+               "value_noself": value_noself, "subgraphs_per_s": subgraphs_per_s,
+               "layer_roofline_frac": layer_roof,
                "setup_s": time.time() - t_setup}
         print(json.dumps(out), flush=True)
     if comm is not None:
