@@ -377,7 +377,7 @@ GSG_API int gsg_subgraph_free(gsg_subgraph_t sg) {
   DeviceGuard dg(sg->device);
   cudaFree(sg->indptr); cudaFree(sg->indices); cudaFree(sg->values);
   cudaFree(sg->rowptr); cudaFree(sg->col); cudaFree(sg->val); cudaFree(sg->valT);
-  cudaFree(sg->perm); cudaFree(sg->rowval); cudaFree(sg->counters);
+  cudaFree(sg->perm); cudaFree(sg->rowval); cudaFree(sg->counters); cudaFree(sg->rowid);
   delete sg;
   return GSG_OK;
 }

@@ -101,6 +101,7 @@ struct gsg_subgraph {
   float* val = nullptr;         // [nnz_hat]
   float* valT = nullptr;        // [nnz_hat]
   int32_t* perm = nullptr;      // [n] rows by descending degree bucket
+  int32_t* rowid = nullptr;     // [nnz] row of each raw entry (normalize scratch)
   float* rowval = nullptr;      // [n] per-row value of the degree modes (1/(d+1) or 1/d), fp64-rounded
   int32_t* counters = nullptr;  // [kBins + 8]: bucket counts ..., [kBins]=n_heavy, [kBins+1]=max_deg
   size_t cap_hat = 0;

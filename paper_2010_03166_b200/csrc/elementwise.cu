@@ -33,7 +33,7 @@ __global__ void k_mask(int rows, int cols4, const float4* __restrict__ dH, int64
 }
 
 constexpr int kHeadThreads = 256;
-constexpr int kHeadBlocks = 256;  // fixed grid -> fixed reduction order (deterministic loss)
+constexpr int kHeadBlocks = 1184;  // fixed grid (8 per SM of 148) -> fixed reduction order (deterministic loss)
 
 // One warp per row. S+ = ReLU(S); Y = softmax(S+) or sigmoid(S+); per-row CE; dS = (Y-Ybar)/n ⊙ 1[S>0].
 __global__ void __launch_bounds__(kHeadThreads) k_head(int n, int C, int kind, const float* __restrict__ S, int64_t lds,
@@ -50,15 +50,18 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(int n, int C, int kind, c
     const float inv_n = node_w ? node_w[i] : 1.0f / (float)n;  // λ_i (GraphSAINT) or 1/n
     if (kind == GSG_HEAD_SOFTMAX) {
       float mx = 0.f;  // S+ >= 0
+#pragma unroll 4
       for (int c = lane; c < C; c += 32) mx = fmaxf(mx, fmaxf(s[c], 0.f));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       float z = 0.f;
+#pragma unroll 4
       for (int c = lane; c < C; c += 32) z += expf(fmaxf(s[c], 0.f) - mx);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
       const float lse = mx + logf(z);
       const int y = cls[i];
+#pragma unroll 4
       for (int c = lane; c < C; c += 32) {
         const float sv = s[c];
         const float p = expf(fmaxf(sv, 0.f) - lse);
@@ -66,6 +69,7 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(int n, int C, int kind, c
       }
       if (lane == 0) acc += inv_n * (lse - fmaxf(s[y], 0.f));
     } else {
+#pragma unroll 4
       for (int c = lane; c < C; c += 32) {
         const float sv = s[c];
         const float sp = fmaxf(sv, 0.f);
@@ -87,13 +91,20 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(int n, int C, int kind, c
   }
 }
 
-// One warp, fixed order: lane l sums partials l, l+32, ... then a fixed xor-tree (deterministic).
-__global__ void k_head_final(int nblocks, int n, const float* __restrict__ partial, float* __restrict__ loss) {
+// One block, fixed order: thread t sums partials t, t + 1024, ... in fp64, then a fixed
+// shared-memory tree (deterministic).
+__global__ void __launch_bounds__(1024) k_head_final(int nblocks, int n, const float* __restrict__ partial,
+                                                     float* __restrict__ loss) {
+  __shared__ double sm[1024];
   double t = 0.0;
-  for (int b = threadIdx.x; b < nblocks; b += 32) t += partial[b];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  if (threadIdx.x == 0) *loss = (float)t;
+  for (int b = threadIdx.x; b < nblocks; b += 1024) t += partial[b];
+  sm[threadIdx.x] = t;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = (float)sm[0];
   (void)n;
 }
 
@@ -127,7 +138,7 @@ int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64
                                                         kind == GSG_HEAD_SOFTMAX ? (const int32_t*)labels : nullptr,
                                                         kind == GSG_HEAD_SIGMOID ? (const uint8_t*)labels : nullptr,
                                                         node_w, dS, part);
-  k_head_final<<<1, 32, 0, ctx->stream>>>(kHeadBlocks, n, part, loss);
+  k_head_final<<<1, 1024, 0, ctx->stream>>>(kHeadBlocks, n, part, loss);
   count_launch(ctx, 2);
   GSG_CUDA(cudaGetLastError());
   return GSG_OK;

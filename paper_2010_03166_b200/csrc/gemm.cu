@@ -821,7 +821,8 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   if (rc) return rc;
   // epilogue store map: C itself, or the split-K workspace [splits * mpad x ldws]
   CUtensorMap mc;
-  g.tma_store = accumulate ? 0 : 1;
+  static const int no_tma_store = getenv("GSG_GEMM_NO_TMA_STORE") ? atoi(getenv("GSG_GEMM_NO_TMA_STORE")) : 0;
+  g.tma_store = (accumulate || no_tma_store) ? 0 : 1;
   if (g.splits > 1) rc = make_store_map(&mc, g.ws, (int64_t)g.splits * g.mpad, N, g.ldws);
   else rc = make_store_map(&mc, Cp, M, N, ldc);
   if (rc) return rc;

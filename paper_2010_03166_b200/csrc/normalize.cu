@@ -34,58 +34,47 @@ __global__ void k_rowptr(int n, const int64_t* __restrict__ indptr, int self, in
   if (threadIdx.x == 0) atomicMax(&counters[kBins + 1], mx);
 }
 
-// Edge-parallel fill: every raw entry k is placed at its slot of Â, shifted by one past the
-// row's self loop, and given the values of the requested normalization in fp64 (rounded once to
-// fp32). Each thread takes kFillPer entries strided by the grid's thread count (coalesced) and
-// finds each entry's row by a binary search of indptr (20K-row indptr is L1/L2-resident), so no
-// row's length serializes the kernel (a warp-per-row loop spent ~45 us on the 1.3K-degree hubs
-// of config 5). The self loops are written by k_fill_self.
+// Row of every raw entry: one warp per row writes its id over [indptr[i], indptr[i+1]) --
+// stores only, so a 1.3K-degree hub row costs ~42 warp-wide stores, not a dependent chain.
+__global__ void k_rowid(int n, const int64_t* __restrict__ indptr, int32_t* __restrict__ rowid) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const int64_t b = indptr[i], e = indptr[i + 1];
+    for (int64_t k = b + lane; k < e; k += 32) rowid[k] = i;
+  }
+}
+
+// Edge-parallel fill: every raw entry k of row r goes to its slot of Â, shifted by one past the
+// row's self loop: rowptr[r] + (k - indptr[r]) + [j > r], i.e. k + r + [j > r] in the self
+// modes (rowptr[r] = indptr[r] + r) and k otherwise -- no per-row serialization (a warp-per-row
+// loop spent ~45 us on the 1.3K-degree hub rows of config 5). Values of the requested
+// normalization are computed in fp64 and rounded once to fp32. k_fill_self writes the loops.
 //
 // For the degree-based modes the transposed value is a closed form of the column's degree
 // (Âᵀ_ij = Â_ji: 1/(d_j+1) row-self, 1/d_j row, val itself for the symmetric mode), written
 // here in the same fp64 -> fp32 rounding as Â_ji, so valT is bit-for-bit the permutation of
 // val that Alg. 4 produces. GSG_NORM_VALUES needs the search (k_transpose_vals).
-constexpr int kFillPer = 4;
-__device__ __forceinline__ int row_of(const int64_t* __restrict__ indptr, int n, int64_t k) {
-  int lo = 0, hi = n - 1;  // largest i with indptr[i] <= k (k < nnz, so a non-empty row)
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(indptr + mid) <= k) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-__global__ void k_fill(int n, int64_t nnz, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                       const float* __restrict__ values, int mode, const int32_t* __restrict__ rowptr,
+__global__ void k_fill(int64_t nnz, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                       const float* __restrict__ values, int mode, const int32_t* __restrict__ rowid,
                        const float* __restrict__ rowval, int32_t* __restrict__ col, float* __restrict__ val,
                        float* __restrict__ valT) {
   const int self = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_SYM_SELF);
   const bool by_row = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_ROW);
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < nnz; k0 += T * kFillPer) {
-    int i[kFillPer], j[kFillPer];
-#pragma unroll
-    for (int u = 0; u < kFillPer; u++) {
-      const int64_t k = k0 + u * T;
-      i[u] = k < nnz ? row_of(indptr, n, k) : 0;
-      j[u] = k < nnz ? __ldg(indices + k) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < kFillPer; u++) {
-      const int64_t k = k0 + u * T;
-      if (k >= nnz) break;
-      const int r = i[u], c = j[u];
-      const int64_t pos = (int64_t)rowptr[r] + (k - __ldg(indptr + r)) + (self && c > r ? 1 : 0);
-      col[pos] = c;
-      if (by_row) {                          // Â_rc = rowval[r], Âᵀ_rc = Â_cr = rowval[c]
-        val[pos] = __ldg(rowval + r);
-        valT[pos] = __ldg(rowval + c);
-      } else if (mode == GSG_NORM_SYM_SELF) {
-        const double dr = (double)(__ldg(indptr + r + 1) - __ldg(indptr + r));
-        const double dc = (double)(__ldg(indptr + c + 1) - __ldg(indptr + c));
-        val[pos] = valT[pos] = (float)(1.0 / sqrt((dr + 1.0) * (dc + 1.0)));
-      } else {
-        val[pos] = values[k];                // GSG_NORM_VALUES: valT by k_transpose_vals
-      }
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += T) {
+    const int r = __ldg(rowid + k), c = __ldg(indices + k);
+    const int64_t pos = self ? k + r + (c > r ? 1 : 0) : k;
+    col[pos] = c;
+    if (by_row) {                          // Â_rc = rowval[r], Âᵀ_rc = Â_cr = rowval[c]
+      val[pos] = __ldg(rowval + r);
+      valT[pos] = __ldg(rowval + c);
+    } else if (mode == GSG_NORM_SYM_SELF) {
+      const double dr = (double)(__ldg(indptr + r + 1) - __ldg(indptr + r));
+      const double dc = (double)(__ldg(indptr + c + 1) - __ldg(indptr + c));
+      val[pos] = valT[pos] = (float)(1.0 / sqrt((dr + 1.0) * (dc + 1.0)));
+    } else {
+      val[pos] = values[k];                // GSG_NORM_VALUES: valT by k_transpose_vals
     }
   }
 }
@@ -182,12 +171,13 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   const int n = sg->n;
   cudaStream_t st = ctx->stream;
   if ((size_t)nh > sg->cap_hat) {
-    cudaFree(sg->col); cudaFree(sg->val); cudaFree(sg->valT);
-    sg->col = nullptr; sg->val = sg->valT = nullptr;
+    cudaFree(sg->col); cudaFree(sg->val); cudaFree(sg->valT); cudaFree(sg->rowid);
+    sg->col = sg->rowid = nullptr; sg->val = sg->valT = nullptr;
     size_t c = (size_t)(nh > 0 ? nh : 1);
     GSG_CUDA(cudaMalloc(&sg->col, c * sizeof(int32_t)));
     GSG_CUDA(cudaMalloc(&sg->val, c * sizeof(float)));
     GSG_CUDA(cudaMalloc(&sg->valT, c * sizeof(float)));
+    GSG_CUDA(cudaMalloc(&sg->rowid, c * sizeof(int32_t)));
     sg->cap_hat = c;
   }
   sg->nnz_hat = nh;
@@ -203,11 +193,12 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
     int wgrid = (int)(((int64_t)n * 32 + T - 1) / T);
     if (wgrid > ctx->num_sms * 16) wgrid = ctx->num_sms * 16;
     if (sg->nnz > 0) {
-      int64_t eg = (sg->nnz + (int64_t)T * kFillPer - 1) / ((int64_t)T * kFillPer);
-      if (eg > (int64_t)ctx->num_sms * 8) eg = (int64_t)ctx->num_sms * 8;
-      k_fill<<<(int)eg, T, 0, st>>>(n, sg->nnz, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode,
-                                    sg->rowptr, sg->rowval, sg->col, sg->val, sg->valT);
-      count_launch(ctx);
+      k_rowid<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->rowid);
+      int64_t eg = (sg->nnz + T - 1) / T;
+      if (eg > (int64_t)ctx->num_sms * 16) eg = (int64_t)ctx->num_sms * 16;
+      k_fill<<<(int)eg, T, 0, st>>>(sg->nnz, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode,
+                                    sg->rowid, sg->rowval, sg->col, sg->val, sg->valT);
+      count_launch(ctx, 2);
     }
     if (self) {
       k_fill_self<<<grid, T, 0, st>>>(n, sg->indptr, sg->indices, sg->rowptr, sg->col, sg->val, sg->valT);

@@ -1,5 +1,6 @@
-"""Measurement tool: one gsg_gemm shape launched eagerly ITERS times (for ncu captures and quick
-A/B timing). SHAPE = "M,N,K,transA,transB", PREC = tf32 | bf16. Prints device us per call."""
+"""Measurement tool: one gsg_gemm shape, ITERS calls captured in a CUDA graph and replayed (device
+time per call without host launch gaps; GRAPH=0 launches eagerly, e.g. under ncu).
+SHAPE = "M,N,K,transA,transB", PREC = tf32 | bf16, EPI = none | relu | mask."""
 import os
 import sys
 
@@ -29,18 +30,36 @@ def main():
         kw["aux"] = pad(M, N, torch.float32)
     stream = torch.cuda.Stream()
     ctx = gsg.Context(0, stream)
+    graph = os.environ.get("GRAPH", "1") == "1"
+
+    def run():
+        ctx.gemm(A, B, C, transA=bool(ta), transB=bool(tb), precision=prec, K=K, **kw)
     with torch.cuda.stream(stream):
         for _ in range(3):
-            ctx.gemm(A, B, C, transA=bool(ta), transB=bool(tb), precision=prec, K=K, **kw)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(iters):
-            ctx.gemm(A, B, C, transA=bool(ta), transB=bool(tb), precision=prec, K=K, **kw)
-        b.record()
+            run()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(iters):
+                run()
+        g.replay()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            a.record()
+            g.replay()
+            b.record()
+    else:
+        with torch.cuda.stream(stream):
+            a.record()
+            for _ in range(iters):
+                run()
+            b.record()
     torch.cuda.synchronize()
     us = a.elapsed_time(b) / iters * 1e3
     print(f"SHAPE={M},{N},{K},{ta},{tb} PREC={os.environ.get('PREC', 'tf32')} EPI={epi}: {us:.2f} us/call "
-          f"{2.0 * M * N * K / us / 1e6:.1f} TFLOP/s (eager, includes host launch gaps)")
+          f"{2.0 * M * N * K / us / 1e6:.1f} TFLOP/s ({'graph replay' if graph else 'eager'})")
 
 
 if __name__ == "__main__":
