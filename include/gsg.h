@@ -178,7 +178,10 @@ GSG_API int gsg_subgraph_free(gsg_subgraph_t sg);
  *   d_Ylp, ldylp optional bf16 copy of Y (NULL = none; ldylp % 8 == 0)
  *   d_mask, ldm  optional ReLU' gate: Y ⊙ 1[mask > 0] (NULL = none) -- used to emit the
  *                next layer's dZ directly from the transposed aggregation
- * Each output row is summed in a fixed order (bitwise reproducible run to run). */
+ * Each output row is summed in a fixed order (bitwise reproducible run to run).
+ * A subgraph with n = 0 returns GSG_OK without reading any pointer. Errors: GSG_EINVAL (not
+ * normalized, f < 1, NULL / misaligned (16 B) pointers, ld < f or ld % 4 != 0, Y aliasing X),
+ * GSG_EUNSUPPORTED (n * ldx * 4 >= 4 GiB: the kernel's 32-bit row byte offsets). */
 GSG_API int gsg_spmm(gsg_ctx_t ctx, gsg_subgraph_t sg, int transpose, int32_t f,
                      const float* d_X, int64_t ldx, float* d_Y, int64_t ldy,
                      void* d_Ylp, int64_t ldylp, const float* d_mask, int64_t ldm);
@@ -194,7 +197,9 @@ GSG_API int gsg_spmm(gsg_ctx_t ctx, gsg_subgraph_t sg, int transpose, int32_t f,
  *   split_k      0 = automatic; >= 1 forces the number of K splits (deterministic fixed-order
  *                reduction through the context workspace)
  *   accumulate   1 = C += result (before the epilogue is NOT supported with RELU/MASK)
- * K = 0 writes epi(0). */
+ * K = 0 writes epi(0); M = 0 or N = 0 returns GSG_OK without reading any pointer. Errors:
+ * GSG_EINVAL (bad precision / epilogue, negative dims, ld or 16-byte alignment violations,
+ * accumulate with an epilogue), GSG_ECUDA (launch failure). */
 GSG_API int gsg_gemm(gsg_ctx_t ctx, int32_t M, int32_t N, int32_t K,
                      const void* d_A, int64_t lda, int transA,
                      const void* d_B, int64_t ldb, int transB,

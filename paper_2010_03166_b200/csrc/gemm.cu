@@ -569,7 +569,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
-// C = epi(sum_s ws[s]) in a fixed split order (deterministic split-K reduction).
+// Epilogue of one reduced float4 (columns c .. c+3 of row; w = valid columns).
+__device__ __forceinline__ void reduce_store4(const GemmArgs& g, int row, int c, int w, const float (&x)[4]) {
+  float* dst = g.C + (int64_t)row * g.ldc + c;
+  for (int j = 0; j < w; j++) {
+    float y = x[j];
+    if (g.accumulate) y += dst[j];
+    if (g.epi == GSG_EPI_RELU) y = fmaxf(y, 0.f);
+    else if (g.epi == GSG_EPI_MASK) y = g.aux[(int64_t)row * g.ldaux + c + j] > 0.f ? y : 0.f;
+    dst[j] = y;
+    if (g.Clp) g.Clp[(int64_t)row * g.ldclp + c + j] = __float2bfloat16_rn(y);
+  }
+}
+
+// C = epi(sum_s ws[s]) in a fixed split order (deterministic split-K reduction), one thread per
+// output float4 (few splits, many outputs).
 __global__ void k_splitk_reduce(GemmArgs g) {
   const int n4 = (g.N + 3) / 4;
   const int64_t total = (int64_t)g.M * n4;
@@ -577,7 +591,6 @@ __global__ void k_splitk_reduce(GemmArgs g) {
     const int row = (int)(i / n4);
     const int c = (int)(i % n4) * 4;
     float x[4] = {0.f, 0.f, 0.f, 0.f};
-    const int w = min(4, g.N - c);
     // ws rows are padded to ldws (multiple of 8 >= N): float4 loads never leave the row. Loads
     // are issued 8 at a time (independent), sums applied in split order (deterministic).
     const float4* p = reinterpret_cast<const float4*>(g.ws + (int64_t)row * g.ldws + c);
@@ -590,19 +603,41 @@ __global__ void k_splitk_reduce(GemmArgs g) {
 #pragma unroll
       for (int u = 0; u < 8; u++) { x[0] += v[u].x; x[1] += v[u].y; x[2] += v[u].z; x[3] += v[u].w; }
     }
-    for (; s < g.splits; s++) {
+    if (s < g.splits) {  // remaining < 8 splits: predicated loads, all in flight together
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) v[u] = s + u < g.splits ? __ldg(p + (s + u) * sstride4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (s + u < g.splits) { x[0] += v[u].x; x[1] += v[u].y; x[2] += v[u].z; x[3] += v[u].w; }
+    }
+    reduce_store4(g, row, c, min(4, g.N - c), x);
+  }
+}
+
+// Same reduction, one warp per output float4 (many splits, few outputs: e.g. a 1024 x 41 head
+// gradient over K = n cut into 64 pieces): lane l sums splits l, l + 32, ... in order, then a
+// fixed xor-butterfly combines the lanes (deterministic; a different but fixed association).
+__global__ void k_splitk_reduce_warp(GemmArgs g) {
+  const int n4 = (g.N + 3) / 4;
+  const int64_t total = (int64_t)g.M * n4;
+  const int lane = threadIdx.x & 31;
+  const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t sstride4 = (int64_t)g.mpad * g.ldws / 4;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += W) {
+    const int row = (int)(i / n4);
+    const int c = (int)(i % n4) * 4;
+    const float4* p = reinterpret_cast<const float4*>(g.ws + (int64_t)row * g.ldws + c);
+    float x[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int s = lane; s < g.splits; s += 32) {
       const float4 v = __ldg(p + s * sstride4);
       x[0] += v.x; x[1] += v.y; x[2] += v.z; x[3] += v.w;
     }
-    float* dst = g.C + (int64_t)row * g.ldc + c;
-    for (int j = 0; j < w; j++) {
-      float y = x[j];
-      if (g.accumulate) y += dst[j];
-      if (g.epi == GSG_EPI_RELU) y = fmaxf(y, 0.f);
-      else if (g.epi == GSG_EPI_MASK) y = g.aux[(int64_t)row * g.ldaux + c + j] > 0.f ? y : 0.f;
-      dst[j] = y;
-      if (g.Clp) g.Clp[(int64_t)row * g.ldclp + c + j] = __float2bfloat16_rn(y);
-    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int j = 0; j < 4; j++) x[j] += __shfl_xor_sync(0xffffffffu, x[j], o);
+    if (lane == 0) reduce_store4(g, row, c, min(4, g.N - c), x);
   }
 }
 
@@ -734,13 +769,13 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   GSG_CHECK(epilogue >= GSG_EPI_NONE && epilogue <= GSG_EPI_MASK, GSG_EINVAL, "bad epilogue %d", epilogue);
   GSG_CHECK(M >= 0 && N >= 0 && K >= 0, GSG_EINVAL, "negative GEMM dims");
   GSG_CHECK(!accumulate || epilogue == GSG_EPI_NONE, GSG_EINVAL, "accumulate only with GSG_EPI_NONE");
+  if (M == 0 || N == 0) return GSG_OK;  // nothing to write: no pointer is read
   GSG_CHECK(Cp && ldc >= N && ldc % 4 == 0 && (uintptr_t)Cp % 16 == 0, GSG_EINVAL,
             "C: need ldc >= N, ldc %% 4 == 0, 16B alignment (ldc=%lld N=%d)", (long long)ldc, N);
   GSG_CHECK(!Clp || (ldclp >= N && ldclp % 8 == 0 && (uintptr_t)Clp % 16 == 0), GSG_EINVAL,
             "Clp: need ldclp >= N, ldclp %% 8 == 0, 16B alignment");
   GSG_CHECK(epilogue != GSG_EPI_MASK || (aux && ldaux >= N && ldaux % 4 == 0 && (uintptr_t)aux % 16 == 0),
             GSG_EINVAL, "EPI_MASK needs aux with ldaux >= N, ldaux %% 4 == 0, 16B alignment");
-  if (M == 0 || N == 0) return GSG_OK;
   const bool bf16 = precision == GSG_PREC_BF16;
   ProfScope ps(ctx, GSG_K_GEMM,
                (double)(bf16 ? 2 : 4) * ((double)M * K + (double)K * N) + 4.0 * M * N, 2.0 * M * N * K);
@@ -821,8 +856,7 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   if (rc) return rc;
   // epilogue store map: C itself, or the split-K workspace [splits * mpad x ldws]
   CUtensorMap mc;
-  static const int no_tma_store = getenv("GSG_GEMM_NO_TMA_STORE") ? atoi(getenv("GSG_GEMM_NO_TMA_STORE")) : 0;
-  g.tma_store = (accumulate || no_tma_store) ? 0 : 1;
+  g.tma_store = accumulate ? 0 : 1;
   if (g.splits > 1) rc = make_store_map(&mc, g.ws, (int64_t)g.splits * g.mpad, N, g.ldws);
   else rc = make_store_map(&mc, Cp, M, N, ldc);
   if (rc) return rc;
@@ -846,10 +880,16 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   }
   if (rc) return rc;
   if (g.splits > 1) {
-    int64_t total = (int64_t)M * ((N + 3) / 4);
-    int grid = (int)((total + 255) / 256);
-    if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
-    k_splitk_reduce<<<grid, 256, 0, ctx->stream>>>(g);
+    const int64_t total = (int64_t)M * ((N + 3) / 4);
+    if (g.splits >= 16 && total < (int64_t)ctx->num_sms * 256) {
+      int64_t grid = (total * 32 + 255) / 256;  // one warp per output float4
+      if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
+      k_splitk_reduce_warp<<<(int)grid, 256, 0, ctx->stream>>>(g);
+    } else {
+      int grid = (int)((total + 255) / 256);
+      if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
+      k_splitk_reduce<<<grid, 256, 0, ctx->stream>>>(g);
+    }
     count_launch(ctx);
     GSG_CUDA(cudaGetLastError());
   }

@@ -329,6 +329,7 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
                 int accum) {
   GSG_CHECK(sg->norm_mode >= 0, GSG_EINVAL, "subgraph not normalized (call gsg_subgraph_normalize)");
   GSG_CHECK(f >= 1, GSG_EINVAL, "f must be >= 1 (got %d)", f);
+  if (sg->n == 0) return GSG_OK;
   GSG_CHECK(X && Y, GSG_EINVAL, "X and Y must be non-NULL");
   GSG_CHECK(ldx >= f && ldx % 4 == 0, GSG_EINVAL, "ldx=%lld must be >= f=%d and a multiple of 4", (long long)ldx, f);
   GSG_CHECK(ldy >= f && ldy % 4 == 0, GSG_EINVAL, "ldy=%lld must be >= f=%d and a multiple of 4", (long long)ldy, f);
@@ -340,7 +341,6 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   GSG_CHECK(X != Y, GSG_EINVAL, "Y must not alias X");
   GSG_CHECK((int64_t)sg->n * ldx * 4 < ((int64_t)1 << 32), GSG_EUNSUPPORTED,
             "X too large for 32-bit byte offsets (n * ldx * 4 >= 4 GiB)");
-  if (sg->n == 0) return GSG_OK;
   // algorithmic (effective gather) bytes, SURVEY §8(d)
   const double nh = (double)sg->nnz_hat, nn = (double)sg->n;
   ProfScope ps(ctx, GSG_K_SPMM, 4.0 * nh * f + 8.0 * nh + 4.0 * (nn + 1) + 4.0 * nn * f, 2.0 * nh * f);

@@ -9,5 +9,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 for s in "20000,1024,200,0,0:relu" "20000,200,1024,0,1:mask" "20000,107,1024,0,0:relu" "20000,1024,1024,0,0:relu"; do
   sh=${s%%:*}; ep=${s##*:}; tag=$(echo $sh | tr ',' '_')
   SHAPE=$sh EPI=$ep timeout 120 python tools/gemm_one.py
-  SHAPE=$sh EPI=$ep ITERS=4 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 3 -c 1 -f -o gpurun_out/gemm_$tag python tools/gemm_one.py > gpurun_out/ncu_gemm_$tag.log 2>&1; echo ncu_$tag=$?
+  SHAPE=$sh EPI=$ep ITERS=4 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 3 -c 1 -f -o gpurun_out/gemm_$tag env GRAPH=0 python tools/gemm_one.py > gpurun_out/ncu_gemm_$tag.log 2>&1; echo ncu_$tag=$?
 done

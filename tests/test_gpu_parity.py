@@ -185,6 +185,40 @@ def test_spmm_deterministic_and_identity(ctx):
     assert np.array_equal(host(Yi), Xi.astype(np.float64))
 
 
+def test_spmm_edge_cases(ctx):
+    """Degenerate and boundary inputs: a subgraph with no nodes, a single node, argument errors
+    (stride / alignment / aliasing) and the 32-bit byte-offset limit (n * ldx * 4 >= 4 GiB is
+    refused with GSG_EUNSUPPORTED before anything is read)."""
+    z = ctx.upload(np.zeros(1, np.int64), np.zeros(0, np.int32)).normalize()
+    X0 = torch.zeros((0, 64), device="cuda")
+    ctx.spmm(z, X0, torch.zeros((0, 64), device="cuda"))                    # n = 0: no-op
+    one = ctx.upload(np.zeros(2, np.int64), np.zeros(0, np.int32)).normalize()
+    X1 = dev(np.full((1, 300), 3.0, np.float32))
+    Y1 = empty(1, 300)
+    ctx.spmm(one, X1, Y1)
+    assert np.array_equal(host(Y1), np.full((1, 300), 3.0))               # Â = [1]
+    g = graph(3000, 10.0, 500, 60, 13)
+    sg = ctx.upload(g.indptr, g.indices).normalize()
+    X = dev(np.ones((g.n, 64), np.float32))
+    with pytest.raises(gsg.GsgError) as e:                                  # aliasing
+        ctx.spmm(sg, X, X)
+    assert e.value.code == gsg.GSG_EINVAL
+    buf = torch.zeros(64 * g.n + 8, device="cuda")
+    with pytest.raises(gsg.GsgError) as e:                                  # 16-byte alignment
+        gsg.check(gsg.gsg_spmm(ctx.h, sg.h, 0, 64, buf.data_ptr() + 4, 64, empty(g.n, 64).data_ptr(), 64,
+                               None, 0, None, 0))
+    assert e.value.code == gsg.GSG_EINVAL
+    with pytest.raises(gsg.GsgError) as e:                                  # ld < f
+        gsg.check(gsg.gsg_spmm(ctx.h, sg.h, 0, 64, buf.data_ptr(), 60, empty(g.n, 64).data_ptr(), 64,
+                               None, 0, None, 0))
+    assert e.value.code == gsg.GSG_EINVAL
+    big = ctx.upload(np.zeros((1 << 20) + 1, np.int64), np.zeros(0, np.int32)).normalize()
+    with pytest.raises(gsg.GsgError) as e:                                  # 2^20 rows x 1024 x 4 B = 4 GiB
+        gsg.check(gsg.gsg_spmm(ctx.h, big.h, 0, 1024, buf.data_ptr(), 1024, buf.data_ptr() + 4096, 1024,
+                               None, 0, None, 0))
+    assert e.value.code == gsg.GSG_EUNSUPPORTED
+
+
 # ------------------------------------------------------------------------------ GEMMs
 GEMM_SHAPES = [(128, 128, 32), (300, 200, 50), (1000, 512, 602), (130, 17, 5), (602, 512, 3000), (64, 1024, 1024),
                (2000, 107, 1024)]
@@ -211,6 +245,25 @@ def test_gemm_vs_oracle(ctx, prec, ta, tb, M, N, K):
     C = empty(M, N)
     ctx.gemm(Ad, Bd, C, transA=ta, transB=tb, precision=prec, K=K)
     assert rel_err(host(C), ref) <= GEMM_TOL
+
+
+@pytest.mark.parametrize("split,ta", [(16, True), (40, True), (64, False)])
+def test_gemm_splitk_many(ctx, split, ta):
+    """Many K pieces and few outputs (head-gradient shapes, dW_mlp = H_L^T dS over K = n): the
+    warp-per-output reduction, with the gate and bf16-copy epilogues, deterministic."""
+    rng = np.random.default_rng(split)
+    M, N, K = 512, 41, 8000
+    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    aux = rng.standard_normal((M, N)).astype(np.float32)
+    ref = orc.gemm(A, B, ta, False)
+    C, C2 = empty(M, N), empty(M, N)
+    Clp = torch.zeros((M, wl.ld_for(N, 8)), dtype=torch.bfloat16, device="cuda")[:, :N]
+    ctx.gemm(dev(A), dev(B), C, transA=ta, epilogue=gsg.GSG_EPI_MASK, aux=dev(aux), Clp=Clp, split_k=split, K=K)
+    assert rel_err(host(C), np.where(aux > 0, ref, 0)) <= GEMM_TOL
+    assert np.array_equal(host(Clp), torch.from_numpy(host(C).astype(np.float32)).bfloat16().float().numpy())
+    ctx.gemm(dev(A), dev(B), C2, transA=ta, epilogue=gsg.GSG_EPI_MASK, aux=dev(aux), split_k=split, K=K)
+    assert torch.equal(C, C2)
 
 
 @pytest.mark.parametrize("split", [1, 3, 7])
@@ -244,6 +297,10 @@ def test_gemm_k0(ctx):
     A = empty(5, 4)
     ctx.gemm(A, A, C, K=0, M=5, N=6)
     assert not host(C).any()
+    # M = 0 or N = 0: nothing to write, no pointer read (NULL accepted)
+    for M, N in ((0, 16), (16, 0)):
+        gsg.check(gsg.gsg_gemm(ctx.h, M, N, 32, None, 32, 0, None, 16, 0, None, 16, None, 0,
+                               gsg.GSG_PREC_TF32, gsg.GSG_EPI_RELU, None, 0, 0, 0))
 
 
 # ------------------------------------------------------------------------------ layer
