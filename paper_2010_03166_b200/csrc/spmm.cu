@@ -6,11 +6,13 @@
 //     SAME column slab at a time so the slab is shared through the 126 MB L2: tasks are
 //     ordered chunk-major (all rows of column chunk 0, then chunk 1, ...), so the concurrently
 //     running warps touch one n x 256-column slab (20 MB at n = 20,000).
-//   * A warp task is one (row, <= 256-column chunk) pair; lane l owns float4 columns l and
-//     l + 32 of the chunk (V = 2), so every neighbor costs one 32-bit offset broadcast and two
-//     coalesced 512-byte row gathers. Neighbor (offset, value) pairs are staged 32 at a time in
-//     shared memory and read back as 128-bit broadcasts (two pairs per LDS.128); 8 neighbors'
-//     gathers (16 x 16 B per lane) are in flight per iteration; accumulation uses packed
+//   * A warp task is one (row, <= 256-column chunk) pair; lane l owns the float4 column pair
+//     2l, 2l + 1 of the chunk, so every neighbor costs one 32-bit offset broadcast and ONE
+//     coalesced 1 KB row gather (LDG.E.256) -- when X is 32-byte aligned with ldx % 8 == 0;
+//     otherwise lane l owns float4 columns l and l + 32 and gathers with two LDG.128.
+//     Neighbor (offset, value) pairs are staged 32 at a time in shared memory and read back as
+//     128-bit broadcasts (two pairs per LDS.128); 8 neighbors' gathers (8 KB per warp) are in
+//     flight per iteration; accumulation uses packed
 //     fp32x2 FMAs (FFMA2). The kernel is bound by L2->SM gather throughput (X is L2-resident),
 //     so instructions per gathered byte are what the design minimizes.
 //   * Degree bins (built by normalize): rows are visited in descending degree order, and
@@ -21,6 +23,8 @@
 //     from device counters, so the launch needs no host synchronization.
 // Every output row is accumulated in a fixed order -> bitwise reproducible.
 #include <cuda_bf16.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -45,6 +49,7 @@ struct SpmmArgs {
   int64_t ldm4;
   const int32_t* __restrict__ perm;
   const int32_t* __restrict__ n_heavy_ptr;
+  int w256;                  // 1: lanes gather 32-byte column pairs with 256-bit loads (X 32-B aligned, ldx % 8 == 0)
 };
 
 constexpr int kWarps = 8;
@@ -125,6 +130,49 @@ __device__ __forceinline__ void warp_row_sum(const SpmmArgs& a, int2* __restrict
       float4 x[V];
       x[0] = __ldg(row_ptr(X, (uint32_t)p.x + lo0));
       if (V == 2) x[1] = __ldg(row_ptr(X, (uint32_t)p.x + lo1));
+      acc_fma(A, __int_as_float(p.y), x);
+    }
+    __syncwarp();
+  }
+}
+
+// One 256-bit gather (LDG.E.256): the lane's two adjacent float4 columns of one X row.
+__device__ __forceinline__ void ld256(const void* p, float4 (&x)[2]) {
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(x[0].x), "=f"(x[0].y), "=f"(x[0].z), "=f"(x[0].w), "=f"(x[1].x), "=f"(x[1].y), "=f"(x[1].z),
+        "=f"(x[1].w)
+      : "l"(p));
+}
+
+// warp_row_sum with 256-bit gathers: lane l owns float4 columns 2l and 2l + 1 of the chunk
+// (lo = byte offset of that pair; idle lanes re-read the chunk's last pair), so a 1 KB chunk
+// row is ONE warp-wide load instruction instead of two 512-byte ones -- half the load
+// instructions and L1 requests per gathered byte, same bytes and registers in flight.
+__device__ __forceinline__ void warp_row_sum256(const SpmmArgs& a, int2* __restrict__ st, int b, int e, uint32_t lo,
+                                                int lane, Acc& A) {
+  const char* X0 = reinterpret_cast<const char*>(a.X) + lo;
+#pragma unroll
+  for (int q = 0; q < 2 * V; q++) A.v[q] = make_float2(0.f, 0.f);
+  for (int k0 = b; k0 < e; k0 += 32) {
+    const int k = k0 + lane;
+    if (k < e) st[lane] = make_int2((int)((uint32_t)__ldg(a.col + k) * a.ldx16), __float_as_int(__ldg(a.val + k)));
+    __syncwarp();
+    const int cnt = min(32, e - k0);
+    int j = 0;
+    for (; j + U <= cnt; j += U) {
+      int4 p[U / 2];
+#pragma unroll
+      for (int q = 0; q < U / 2; q++) p[q] = reinterpret_cast<const int4*>(st)[(j >> 1) + q];
+      float4 x[U][V];
+#pragma unroll
+      for (int u = 0; u < U; u++) ld256(X0 + ((u & 1) ? (uint32_t)p[u >> 1].z : (uint32_t)p[u >> 1].x), x[u]);
+#pragma unroll
+      for (int u = 0; u < U; u++) acc_fma(A, __int_as_float((u & 1) ? p[u >> 1].w : p[u >> 1].y), x[u]);
+    }
+    for (; j < cnt; j++) {
+      const int2 p = st[j];
+      float4 x[V];
+      ld256(X0 + (uint32_t)p.x, x);
       acc_fma(A, __int_as_float(p.y), x);
     }
     __syncwarp();
@@ -219,14 +267,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
     const int b = a.rowptr[row], e = a.rowptr[row + 1];
     const int seg = (e - b + kWarps - 1) / kWarps;
     const int w0 = min(e, b + warp * seg), w1 = min(e, w0 + seg);
-    const int c4 = chunk * a.cw + lane;
-    const int lim = min(a.f4, (chunk + 1) * a.cw);
-    const bool act0 = c4 < lim, act1 = c4 + 32 < lim;
+    const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
+    int c4, c4b;  // output float4 columns of acc_part(A, 0) and acc_part(A, 1)
     Acc A;
-    if (a.cw == 32 * V && lim == (chunk + 1) * a.cw)
-      warp_row_sum<true>(a, st, w0, w1, 16u * c4, 16u * (c4 + 32), lane, A);
-    else
-      warp_row_sum<false>(a, st, w0, w1, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
+    if (a.w256) {
+      c4 = c0 + 2 * lane;
+      c4b = c4 + 1;
+      warp_row_sum256(a, st, w0, w1, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
+    } else {
+      c4 = c0 + lane;
+      c4b = c4 + 32;
+      if (a.cw == 32 * V && lim == (chunk + 1) * a.cw)
+        warp_row_sum<true>(a, st, w0, w1, 16u * c4, 16u * (c4 + 32), lane, A);
+      else
+        warp_row_sum<false>(a, st, w0, w1, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
+    }
+    const bool act0 = c4 < lim, act1 = c4b < lim;
     part[warp][lane] = acc_part(A, 0);
     part[warp][lane + 32] = acc_part(A, 1);
     __syncthreads();
@@ -239,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
           const float4 p = part[w][lane + 32 * q];
           s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
         }
-        if (q == 0 ? act0 : act1) store_row(a, row, c4 + 32 * q, s);
+        if (q == 0 ? act0 : act1) store_row(a, row, q == 0 ? c4 : c4b, s);
       }
     }
     __syncthreads();
@@ -252,17 +308,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
   for (int64_t t = gw; t < L; t += GW) {
     const int chunk = (int)(t / n_light);
     const int row = a.perm[n_heavy + (int)(t % n_light)];
-    const int c4 = chunk * a.cw + lane;
-    const int lim = min(a.f4, (chunk + 1) * a.cw);
-    const bool act0 = c4 < lim, act1 = c4 + 32 < lim;
-    Acc A;
+    const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
     const int b = a.rowptr[row], e = a.rowptr[row + 1];
-    if (a.cw == 32 * V && lim == (chunk + 1) * a.cw)
-      warp_row_sum<true>(a, st, b, e, 16u * c4, 16u * (c4 + 32), lane, A);
-    else
-      warp_row_sum<false>(a, st, b, e, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
-    if (act0) store_row(a, row, c4, acc_part(A, 0));
-    if (act1) store_row(a, row, c4 + 32, acc_part(A, 1));
+    int c4, c4b;
+    Acc A;
+    if (a.w256) {
+      c4 = c0 + 2 * lane;
+      c4b = c4 + 1;
+      warp_row_sum256(a, st, b, e, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
+    } else {
+      c4 = c0 + lane;
+      c4b = c4 + 32;
+      if (a.cw == 32 * V && lim == (chunk + 1) * a.cw)
+        warp_row_sum<true>(a, st, b, e, 16u * c4, 16u * (c4 + 32), lane, A);
+      else
+        warp_row_sum<false>(a, st, b, e, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
+    }
+    if (c4 < lim) store_row(a, row, c4, acc_part(A, 0));
+    if (c4b < lim) store_row(a, row, c4b, acc_part(A, 1));
   }
 }
 
@@ -344,7 +407,7 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   // algorithmic (effective gather) bytes, SURVEY §8(d)
   const double nh = (double)sg->nnz_hat, nn = (double)sg->n;
   ProfScope ps(ctx, GSG_K_SPMM, 4.0 * nh * f + 8.0 * nh + 4.0 * (nn + 1) + 4.0 * nn * f, 2.0 * nh * f);
-  SpmmArgs a;
+  SpmmArgs a{};
   a.n = sg->n;
   a.f4 = (f + 3) / 4;
   a.rowptr = sg->rowptr;
@@ -367,6 +430,10 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   if (a.f4 > 16) {
     a.nchunks = (a.f4 + 32 * V - 1) / (32 * V);
     a.cw = (a.f4 + a.nchunks - 1) / a.nchunks;
+    static int w256_env = -1;
+    if (w256_env < 0) { const char* ev = getenv("GSG_SPMM_W256"); w256_env = ev ? atoi(ev) : 1; }
+    a.w256 = w256_env && (uintptr_t)X % 32 == 0 && ldx % 8 == 0;  // GSG_SPMM_W256=0: 128-bit path (A/B)
+    if (a.w256) a.cw = (a.cw + 1) & ~1;  // chunks start on 32-byte column pairs
     return launch_k(ctx, k_spmm_wide, &occ_wide, a, (int64_t)sg->n * a.nchunks);
   }
   a.nchunks = 1;
