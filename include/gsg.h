@@ -75,11 +75,15 @@ enum {
   GSG_NO_RELU = 1,         /* forward: H = P W (no ReLU)                                   */
   GSG_DH_PREMASKED = 2,    /* backward: dH already equals dZ = dH ⊙ 1[H>0] (fused upstream) */
   GSG_ACCUM_DW = 4,        /* backward: dW += Pᵀ dZ instead of dW = Pᵀ dZ                  */
-  GSG_ORDER_A_XW = 8       /* chain order 2 of §7.1: forward Y = X W then
+  GSG_ORDER_A_XW = 8,      /* chain order 2 of §7.1: forward Y = X W then
                               H = ReLU(Â Y) (the SpMM runs at width f_out); backward
                               G = Âᵀ dZ, dW = Xᵀ G, dX = (G Wᵀ) ⊙ 1[H_below > 0]. With this
                               flag the P arguments of both calls carry X's role: forward
                               writes Y (n x f_out) into P; backward reads X (n x f_in) from P. */
+  GSG_W_BF16 = 16          /* GSG_PREC_BF16 only: d_W already points to a bf16 copy of W
+                              (row-major f_in x f_out, ldw in bf16 elements, ldw % 8 == 0),
+                              e.g. made once per step with gsg_to_bf16 and shared by the
+                              layer's forward and backward; no per-call conversion. */
 };
 
 /* ---- GEMM epilogues (gsg_gemm) ------------------------------------------------------- */
@@ -216,7 +220,8 @@ GSG_API int gsg_to_bf16(gsg_ctx_t ctx, int32_t rows, int32_t cols, const float* 
  *   X (n x f_in, ldx), W (f_in x f_out row-major, ldw), P (n x f_in, ldp), H (n x f_out, ldh)
  *   precision = GSG_PREC_BF16 additionally needs P_lp (bf16 n x f_in, ldplp) which the
  *   aggregation writes for the GEMM; H_lp (bf16 n x f_out) is optional.
- * Chain order (ÂX)W is fixed (SURVEY §8(a) notes; §7.1 P:923-934 order choice is NEXT). */
+ * Chain order: (ÂX)W by default; GSG_ORDER_A_XW selects Â(XW) (§7.1).
+ * BF16: W is converted to bf16 per call unless GSG_W_BF16 says d_W already is bf16. */
 GSG_API int gsg_layer_forward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, int32_t f_out,
                               const float* d_X, int64_t ldx, const float* d_W, int64_t ldw,
                               float* d_P, int64_t ldp, void* d_Plp, int64_t ldplp,

@@ -153,6 +153,25 @@ int nccl_fail(ncclResult_t r, const char* what) {
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+// The bf16 weight operand of a layer GEMM: the caller's own copy (GSG_W_BF16: W is bf16 with
+// ldw in bf16 elements) or a conversion into the context workspace.
+int bf16_weight(gsg_ctx* c, const float* W, int64_t ldw, int f_in, int f_out, int flags, const void** out,
+                int64_t* ld_out) {
+  if (flags & GSG_W_BF16) {
+    GSG_CHECK(ldw >= f_out && ldw % 8 == 0 && (uintptr_t)W % 16 == 0, GSG_EINVAL,
+              "GSG_W_BF16: bf16 W needs ldw >= f_out, ldw %% 8 == 0 and 16-byte alignment");
+    *out = W;
+    *ld_out = ldw;
+    return GSG_OK;
+  }
+  const int64_t ldwl = round_up(f_out, 8);
+  if (int rc = c->ws_lp0.reserve(sizeof(uint16_t) * f_in * ldwl)) return rc;
+  if (int rc = to_bf16_launch(c, f_in, f_out, W, ldw, c->ws_lp0.ptr, ldwl)) return rc;
+  *out = c->ws_lp0.ptr;
+  *ld_out = ldwl;
+  return GSG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -422,12 +441,13 @@ GSG_API int gsg_layer_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
     // chain order 2 (§7.1): Y = X W (into P), H = ReLU(Â Y)
     GSG_CHECK(ldp >= f_out, GSG_EINVAL, "GSG_ORDER_A_XW: P holds Y = X W and needs ldp >= f_out");
     if (precision == GSG_PREC_BF16) {
-      const int64_t ldwl = round_up(f_out, 8), ldxl = round_up(f_in, 8);
-      if ((rc = c->ws_lp0.reserve(sizeof(uint16_t) * f_in * ldwl))) return rc;
+      const int64_t ldxl = round_up(f_in, 8);
+      const void* Wl = nullptr;
+      int64_t ldwl2 = 0;
+      if ((rc = bf16_weight(c, W, ldw, f_in, f_out, flags, &Wl, &ldwl2))) return rc;
       if ((rc = c->ws_lp2.reserve(sizeof(uint16_t) * n * ldxl))) return rc;
-      if ((rc = to_bf16_launch(c, f_in, f_out, W, ldw, c->ws_lp0.ptr, ldwl))) return rc;
       if ((rc = to_bf16_launch(c, n, f_in, X, ldx, c->ws_lp2.ptr, ldxl))) return rc;
-      rc = gemm_launch(c, n, f_out, f_in, c->ws_lp2.ptr, ldxl, 0, c->ws_lp0.ptr, ldwl, 0, P, ldp, nullptr, 0, precision,
+      rc = gemm_launch(c, n, f_out, f_in, c->ws_lp2.ptr, ldxl, 0, Wl, ldwl2, 0, P, ldp, nullptr, 0, precision,
                        GSG_EPI_NONE, nullptr, 0, 0, 0);
     } else {
       rc = gemm_launch(c, n, f_out, f_in, X, ldx, 0, W, ldw, 0, P, ldp, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0,
@@ -440,10 +460,10 @@ GSG_API int gsg_layer_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
   if (rc) return rc;
   const int epi = (flags & GSG_NO_RELU) ? GSG_EPI_NONE : GSG_EPI_RELU;
   if (precision == GSG_PREC_BF16) {
-    const int64_t ldwl = round_up(f_out, 8);
-    if ((rc = c->ws_lp0.reserve(sizeof(uint16_t) * f_in * ldwl))) return rc;
-    if ((rc = to_bf16_launch(c, f_in, f_out, W, ldw, c->ws_lp0.ptr, ldwl))) return rc;
-    return gemm_launch(c, n, f_out, f_in, Plp, ldplp, 0, c->ws_lp0.ptr, ldwl, 0, H, ldh, Hlp, ldhlp, precision, epi,
+    const void* Wl = nullptr;
+    int64_t ldwl = 0;
+    if ((rc = bf16_weight(c, W, ldw, f_in, f_out, flags, &Wl, &ldwl))) return rc;
+    return gemm_launch(c, n, f_out, f_in, Plp, ldplp, 0, Wl, ldwl, 0, H, ldh, Hlp, ldhlp, precision, epi,
                        nullptr, 0, 0, 0);
   }
   return gemm_launch(c, n, f_out, f_in, P, ldp, 0, W, ldw, 0, H, ldh, Hlp, ldhlp, precision, epi, nullptr, 0, 0, 0);
@@ -471,16 +491,19 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   const void* dZlp = dHlp;
   int64_t lddzlp = lddhlp;
   if (!(flags & GSG_DH_PREMASKED)) {
+    // BF16 chain order 1 reads only the bf16 dZ (both GEMMs): the fp32 copy is not written
+    const bool need_fp32 = !bf16 || (flags & GSG_ORDER_A_XW);
     lddz = round_up(f_out, 4);
-    if ((rc = c->ws_dZ.reserve(sizeof(float) * n * lddz))) return rc;
+    if (need_fp32 && (rc = c->ws_dZ.reserve(sizeof(float) * n * lddz))) return rc;
     void* lp = nullptr;
     if (bf16) {
       lddzlp = round_up(f_out, 8);
       if ((rc = c->ws_lp1.reserve(sizeof(uint16_t) * n * lddzlp))) return rc;
       lp = c->ws_lp1.ptr;
     }
-    if ((rc = mask_launch(c, n, f_out, dH, lddh, H, ldh, (float*)c->ws_dZ.ptr, lddz, lp, lddzlp))) return rc;
-    dZ = (const float*)c->ws_dZ.ptr;
+    float* dzo = need_fp32 ? (float*)c->ws_dZ.ptr : nullptr;
+    if ((rc = mask_launch(c, n, f_out, dH, lddh, H, ldh, dzo, lddz, lp, lddzlp))) return rc;
+    dZ = dzo;
     dZlp = lp;
   } else if (bf16 && !dZlp) {
     lddzlp = round_up(f_out, 8);
@@ -501,12 +524,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
     if ((rc = spmm_launch(c, sg, 1, f_out, dZ, lddz, G, ldg, Glp, ldg, nullptr, 0))) return rc;
     const void* Wop2 = W;
     int64_t ldw2 = ldw;
-    if (bf16) {
-      ldw2 = round_up(f_out, 8);
-      if ((rc = c->ws_lp0.reserve(sizeof(uint16_t) * f_in * ldw2))) return rc;
-      if ((rc = to_bf16_launch(c, f_in, f_out, W, ldw, c->ws_lp0.ptr, ldw2))) return rc;
-      Wop2 = c->ws_lp0.ptr;
-    }
+    if (bf16 && (rc = bf16_weight(c, W, ldw, f_in, f_out, flags, &Wop2, &ldw2))) return rc;
     rc = gemm_launch(c, f_in, f_out, n, bf16 ? Plp : (const void*)P, bf16 ? ldplp : ldp, 1, bf16 ? Glp : (const void*)G,
                      ldg, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, (flags & GSG_ACCUM_DW) ? 1 : 0);
     if (rc || !dX) return rc;
@@ -515,12 +533,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   }
   const void* Wop = W;
   int64_t ldwop = ldw;
-  if (bf16) {
-    ldwop = round_up(f_out, 8);
-    if ((rc = c->ws_lp0.reserve(sizeof(uint16_t) * f_in * ldwop))) return rc;
-    if ((rc = to_bf16_launch(c, f_in, f_out, W, ldw, c->ws_lp0.ptr, ldwop))) return rc;
-    Wop = c->ws_lp0.ptr;
-  }
+  if (bf16 && (rc = bf16_weight(c, W, ldw, f_in, f_out, flags, &Wop, &ldwop))) return rc;
   // dW = Pᵀ dZ   (row a5): A = P stored n x f_in (MN-major), B = dZ stored n x f_out (MN-major)
   rc = gemm_launch(c, f_in, f_out, n, bf16 ? Plp : (const void*)P, bf16 ? ldplp : ldp, 1, bf16 ? dZlp : (const void*)dZ,
                    bf16 ? lddzlp : lddz, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0,

@@ -21,7 +21,7 @@ __global__ void k_mask(int rows, int cols4, const float4* __restrict__ dH, int64
     z.y = h.y > 0.f ? g.y : 0.f;
     z.z = h.z > 0.f ? g.z : 0.f;
     z.w = h.w > 0.f ? g.w : 0.f;
-    dZ[(int64_t)r * lddz4 + c] = z;
+    if (dZ) dZ[(int64_t)r * lddz4 + c] = z;
     if (dZlp) {
       __nv_bfloat162 lo = __floats2bfloat162_rn(z.x, z.y), hi = __floats2bfloat162_rn(z.z, z.w);
       uint2 p;
@@ -112,11 +112,11 @@ __global__ void __launch_bounds__(1024) k_head_final(int nblocks, int n, const f
 
 int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh, const float* H, int64_t ldh, float* dZ,
                 int64_t lddz, void* dZlp, int64_t lddzlp) {
-  GSG_CHECK(dH && H && dZ, GSG_EINVAL, "mask: NULL argument");
+  GSG_CHECK(dH && H && (dZ || dZlp), GSG_EINVAL, "mask: NULL argument");
   GSG_CHECK(lddh % 4 == 0 && ldh % 4 == 0 && lddz % 4 == 0 && (!dZlp || lddzlp % 8 == 0), GSG_EINVAL,
             "mask: strides must be multiples of 4 (bf16: 8)");
   if (rows == 0 || cols == 0) return GSG_OK;
-  ProfScope ps(ctx, GSG_K_OTHER, 12.0 * rows * cols, 0.0);
+  ProfScope ps(ctx, GSG_K_OTHER, (8.0 + (dZ ? 4.0 : 0.0) + (dZlp ? 2.0 : 0.0)) * rows * cols, 0.0);
   const int cols4 = (cols + 3) / 4;
   const int64_t total = (int64_t)rows * cols4;
   int grid = (int)((total + 255) / 256);

@@ -17,7 +17,7 @@ from __future__ import annotations
 import torch
 
 from . import (GSG_DH_PREMASKED, GSG_HEAD_SIGMOID, GSG_HEAD_SOFTMAX, GSG_NORM_ROW_SELF, GSG_ORDER_A_XW,
-               GSG_PREC_BF16, GSG_PREC_TF32, Context, Subgraph)
+               GSG_PREC_BF16, GSG_PREC_TF32, GSG_W_BF16, Context, Subgraph)
 
 
 def chain_order(f_in: int, f_out: int) -> int:
@@ -55,6 +55,9 @@ class GCNStep:
         self.H = [padded(n_max, dims[l + 1], device=dev) for l in range(self.L)]
         self.dX = [padded(n_max, dims[l], device=dev) for l in range(self.L)]
         self.Plp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
+        # bf16 weight copies, converted once per step and shared by each layer's forward and
+        # backward GEMMs (GSG_W_BF16) instead of one conversion per GEMM call
+        self.Wlp = [padded(dims[l], dims[l + 1], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
         self.dXlp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
         # all weight gradients in one flat buffer -> one allreduce (a9)
         # (rows padded to 16-byte strides; the padding is reduced along harmlessly)
@@ -83,14 +86,20 @@ class GCNStep:
         ctx, d, n = self.ctx, self.dims, sg.n
         if normalize:
             sg.normalize(GSG_NORM_ROW_SELF)
+        bf = self.prec == GSG_PREC_BF16
+        if bf:
+            for w, wl in zip(self.W, self.Wlp):
+                ctx.to_bf16(w, wl)
+        Wop = self.Wlp if bf else self.W
+        wflag = GSG_W_BF16 if bf else 0
         h = X
         inputs = []
         for l in range(self.L):
             inputs.append(h)
             o2 = self.order[l] == 2
-            ctx.layer_forward(sg, h, self.W[l], self.P[l][:n], self.H[l][:n], d[l], d[l + 1], precision=self.prec,
+            ctx.layer_forward(sg, h, Wop[l], self.P[l][:n], self.H[l][:n], d[l], d[l + 1], precision=self.prec,
                               Plp=None if (self.Plp[l] is None or o2) else self.Plp[l][:n],
-                              flags=GSG_ORDER_A_XW if o2 else 0)
+                              flags=(GSG_ORDER_A_XW if o2 else 0) | wflag)
             h = self.H[l][:n]
         if self.head != "none":
             kind = GSG_HEAD_SOFTMAX if self.head == "softmax" else GSG_HEAD_SIGMOID
@@ -106,10 +115,10 @@ class GCNStep:
             Plp = None if self.Plp[l] is None else self.Plp[l][:n]
             if o2 and Plp is not None:
                 ctx.to_bf16(inputs[l], Plp)
-            ctx.layer_backward(sg, Pl, self.H[l][:n], dH, self.W[l], self.dW[l], self.dX[l][:n],
+            ctx.layer_backward(sg, Pl, self.H[l][:n], dH, Wop[l], self.dW[l], self.dX[l][:n],
                                d[l], d[l + 1], precision=self.prec, Plp=Plp, dHlp=dHlp,
                                dXlp=None if self.dXlp[l] is None else self.dXlp[l][:n], H_below=Hb,
-                               flags=flags | (GSG_ORDER_A_XW if o2 else 0))
+                               flags=flags | (GSG_ORDER_A_XW if o2 else 0) | wflag)
             dH = self.dX[l][:n]
             dHlp = None if self.dXlp[l] is None else self.dXlp[l][:n]
             flags = GSG_DH_PREMASKED  # the transposed aggregation already applied layer l-1's ReLU' gate
