@@ -8,25 +8,54 @@ namespace {
 
 __device__ __forceinline__ int bucket_of(int d) { return d <= 0 ? 0 : 32 - __clz(d); }
 
-// rowptr[i] = indptr[i] + self*i ; histogram of degree buckets ; max degree
-// ... and the per-row value of the degree modes, rowval[i] = fp32(1/(d_i+1)) (row-self) or
-// fp32(1/d_i) (row), reused by k_fill for Â_ij and, gathered at column j, for Âᵀ_ij = Â_ji.
-__global__ void k_rowptr(int n, const int64_t* __restrict__ indptr, int self, int mode, int32_t* __restrict__ rowptr,
-                         float* __restrict__ rowval, int32_t* __restrict__ counters) {
+// One warp per row: rowptr[i] = indptr[i] + self*i, the degree-bucket histogram and max
+// degree, the per-row value of the degree modes (rowval[i] = fp32(1/(d_i+1)) row-self or
+// fp32(1/d_i) row, reused by k_fill for Â_ij and, gathered at column j, for Âᵀ_ij = Â_ji),
+// the row id of every raw entry (for k_fill) and -- self modes -- the self loop itself, placed
+// after the row's neighbors below i (a 32-way warp search of the ascending list: a 1.3K-degree
+// row needs 3 probe rounds; the id stores carry no loads).
+__global__ void k_rows(int n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices, int self,
+                       int mode, int32_t* __restrict__ rowptr, float* __restrict__ rowval,
+                       int32_t* __restrict__ counters, int32_t* __restrict__ rowid, int32_t* __restrict__ col,
+                       float* __restrict__ val, float* __restrict__ valT) {
   __shared__ int hist[kBins];
   __shared__ int mx;
   if (threadIdx.x < kBins) hist[threadIdx.x] = 0;
   if (threadIdx.x == 0) mx = 0;
   __syncthreads();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
-    rowptr[i] = (int32_t)(indptr[i] + (self ? i : 0));
-    if (i < n) {
-      const int d0 = (int)(indptr[i + 1] - indptr[i]);
-      int d = d0 + self;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) rowptr[n] = (int32_t)(indptr[n] + (self ? n : 0));
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    const int64_t b = indptr[i], e = indptr[i + 1];
+    const int d0 = (int)(e - b);
+    for (int64_t k = b + lane; k < e; k += 32) rowid[k] = i;  // stores only
+    int64_t lo = b, hi = e;  // self-loop position: first entry > i, by a 32-way warp search
+    while (self && lo < hi) {
+      const int64_t step = (hi - lo + 31) >> 5;
+      const int64_t pl = lo + lane * step;
+      const unsigned m = __ballot_sync(0xffffffffu, pl < hi && __ldg(indices + pl) > i);
+      if (m) {
+        const int f = __ffs(m) - 1;
+        hi = lo + f * step;
+        lo = f ? lo + (int64_t)(f - 1) * step + 1 : hi;
+      } else {  // every probe <= i: continue after the last probe below hi
+        lo += ((hi - 1 - lo) / step) * step + 1;
+      }
+    }
+    const int below = (int)(lo - b);  // neighbors with id < i
+    if (lane == 0) {
+      const int32_t o = (int32_t)(b + (self ? i : 0));
+      rowptr[i] = o;
+      const int d = d0 + self;
       atomicAdd(&hist[bucket_of(d)], 1);
       atomicMax(&mx, d);
       if (mode == GSG_NORM_ROW_SELF) rowval[i] = (float)(1.0 / ((double)d0 + 1.0));
       else if (mode == GSG_NORM_ROW) rowval[i] = d0 > 0 ? (float)(1.0 / (double)d0) : 0.f;
+      if (self) {  // Â_ii = 1/(d_i+1) (row-self; sym: 1/sqrt((d_i+1)^2))
+        col[o + below] = i;
+        val[o + below] = valT[o + below] = (float)(1.0 / ((double)d0 + 1.0));
+      }
     }
   }
   __syncthreads();
@@ -34,22 +63,11 @@ __global__ void k_rowptr(int n, const int64_t* __restrict__ indptr, int self, in
   if (threadIdx.x == 0) atomicMax(&counters[kBins + 1], mx);
 }
 
-// Row of every raw entry: one warp per row writes its id over [indptr[i], indptr[i+1]) --
-// stores only, so a 1.3K-degree hub row costs ~42 warp-wide stores, not a dependent chain.
-__global__ void k_rowid(int n, const int64_t* __restrict__ indptr, int32_t* __restrict__ rowid) {
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
-    const int64_t b = indptr[i], e = indptr[i + 1];
-    for (int64_t k = b + lane; k < e; k += 32) rowid[k] = i;
-  }
-}
-
 // Edge-parallel fill: every raw entry k of row r goes to its slot of Â, shifted by one past the
 // row's self loop: rowptr[r] + (k - indptr[r]) + [j > r], i.e. k + r + [j > r] in the self
 // modes (rowptr[r] = indptr[r] + r) and k otherwise -- no per-row serialization (a warp-per-row
 // loop spent ~45 us on the 1.3K-degree hub rows of config 5). Values of the requested
-// normalization are computed in fp64 and rounded once to fp32. k_fill_self writes the loops.
+// normalization are computed in fp64 and rounded once to fp32. k_rows writes the self loops.
 //
 // For the degree-based modes the transposed value is a closed form of the column's degree
 // (Âᵀ_ij = Â_ji: 1/(d_j+1) row-self, 1/d_j row, val itself for the symmetric mode), written
@@ -79,24 +97,6 @@ __global__ void k_fill(int64_t nnz, const int64_t* __restrict__ indptr, const in
   }
 }
 
-// Self loops (self modes): row i's loop goes after its neighbors with id < i, found by a binary
-// search of the ascending list; value 1/(d_i+1) (row-self: Â_ii; sym: 1/sqrt((d_i+1)^2)).
-__global__ void k_fill_self(int n, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                            const int32_t* __restrict__ rowptr, int32_t* __restrict__ col, float* __restrict__ val,
-                            float* __restrict__ valT) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int64_t b = indptr[i], e = indptr[i + 1];
-    int64_t lo = b, hi = e;  // first position with indices[pos] > i
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (__ldg(indices + mid) < i) lo = mid + 1; else hi = mid;
-    }
-    const int32_t pos = rowptr[i] + (int32_t)(lo - b);
-    col[pos] = i;
-    val[pos] = valT[pos] = (float)(1.0 / ((double)(e - b) + 1.0));
-  }
-}
-
 // valT at slot (u, v) = val at slot (v, u): binary search for u in row v's ascending list.
 // One warp per row u. This reproduces Alg. 4's DataTrans exactly (same structure, a pure
 // permutation of val).
@@ -122,26 +122,25 @@ __global__ void k_transpose_vals(int n, const int32_t* __restrict__ rowptr, cons
   }
 }
 
-// Exclusive offsets of the buckets in DESCENDING bucket order; n_heavy = rows with
-// deg' >= kHeavyMinDeg (buckets >= bucket_of(kHeavyMinDeg)).
-__global__ void k_bin_offsets(int32_t* counters) {
+// Rows by DESCENDING degree bucket. Every block derives the bucket offsets from the finished
+// histogram itself (exclusive sums in descending bucket order; n_heavy = rows with
+// deg' >= kHeavyMinDeg), then ranks its rows in shared memory and reserves each bucket's range
+// with one global atomic per (block, bucket) on a zeroed cursor (the order within a bucket is
+// immaterial: every row is summed by one warp or CTA in CSR order).
+__global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t* __restrict__ counters,
+                              int32_t* __restrict__ perm) {
+  __shared__ int cnt[kBins], base[kBins], off[kBins];
   if (threadIdx.x == 0) {
     int acc = 0, heavy = 0;
     const int hb = 32 - __clz(kHeavyMinDeg);
     for (int b = kBins - 1; b >= 0; b--) {
-      counters[kBins + 2 + b] = acc;  // cursor start
+      off[b] = acc;
       acc += counters[b];
       if (b >= hb) heavy += counters[b];
     }
-    counters[kBins] = heavy;
+    if (blockIdx.x == 0) counters[kBins] = heavy;
   }
-}
-
-__global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t* __restrict__ counters,
-                              int32_t* __restrict__ perm) {
-  // two-level: shared-memory ranks within the block's slice of rows, then one global atomic per
-  // (block, bucket) to reserve the block's range (the order within a bucket is immaterial)
-  __shared__ int cnt[kBins], base[kBins];
+  __syncthreads();
   for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
     if (threadIdx.x < kBins) cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -153,7 +152,7 @@ __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t
     }
     __syncthreads();
     if (threadIdx.x < kBins && cnt[threadIdx.x])
-      base[threadIdx.x] = atomicAdd(&counters[kBins + 2 + threadIdx.x], cnt[threadIdx.x]);
+      base[threadIdx.x] = off[threadIdx.x] + atomicAdd(&counters[kBins + 2 + threadIdx.x], cnt[threadIdx.x]);
     __syncthreads();
     if (b >= 0) perm[base[b] + r] = i;
     __syncthreads();
@@ -188,31 +187,26 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   int grid = (n + 1 + T - 1) / T;
   if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
   if (grid < 1) grid = 1;
-  k_rowptr<<<grid, T, 0, st>>>(n, sg->indptr, self, mode, sg->rowptr, sg->rowval, sg->counters);
+  int wgrid = (int)(((int64_t)n * 32 + T - 1) / T);
+  if (wgrid > ctx->num_sms * 16) wgrid = ctx->num_sms * 16;
+  if (wgrid < 1) wgrid = 1;
+  k_rows<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->indices, self, mode, sg->rowptr, sg->rowval, sg->counters, sg->rowid,
+                               sg->col, sg->val, sg->valT);
+  count_launch(ctx);
   if (n > 0) {
-    int wgrid = (int)(((int64_t)n * 32 + T - 1) / T);
-    if (wgrid > ctx->num_sms * 16) wgrid = ctx->num_sms * 16;
     if (sg->nnz > 0) {
-      k_rowid<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->rowid);
       int64_t eg = (sg->nnz + T - 1) / T;
       if (eg > (int64_t)ctx->num_sms * 16) eg = (int64_t)ctx->num_sms * 16;
       k_fill<<<(int)eg, T, 0, st>>>(sg->nnz, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode,
                                     sg->rowid, sg->rowval, sg->col, sg->val, sg->valT);
-      count_launch(ctx, 2);
-    }
-    if (self) {
-      k_fill_self<<<grid, T, 0, st>>>(n, sg->indptr, sg->indices, sg->rowptr, sg->col, sg->val, sg->valT);
       count_launch(ctx);
     }
     if (mode == GSG_NORM_VALUES) {
       k_transpose_vals<<<wgrid, T, 0, st>>>(n, sg->rowptr, sg->col, sg->val, sg->valT, sg->counters + 3 * kBins + 4);
       count_launch(ctx);
     }
-    k_bin_offsets<<<1, 32, 0, st>>>(sg->counters);
     k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm);
-    count_launch(ctx, 3);
-  } else {
-    count_launch(ctx, 1);
+    count_launch(ctx);
   }
   GSG_CUDA(cudaGetLastError());
   return GSG_OK;
