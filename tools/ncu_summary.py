@@ -2,6 +2,8 @@
 
   python tools/ncu_summary.py launches <launches.csv>      per-kernel share of device time
   python tools/ncu_summary.py report <file.ncu-rep> [...]  key metrics of each captured launch
+  python tools/ncu_summary.py traffic <spmm_metrics.csv> [k]  DRAM / L2 bytes of the last k (6)
+        SpMM launches (one config-5 step) -> profiles/spmm_traffic.json (bench.py's roofline.traffic)
 """
 import collections
 import csv
@@ -61,9 +63,33 @@ def report(path):
     return res
 
 
+def traffic(path, k=6):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    h, data = rows[hi], rows[hi + 1:]
+    idi, mi, vi, ui = h.index("ID"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "nsecond": 1e-3, "us": 1, "usecond": 1,
+             "ms": 1e3, "msecond": 1e3}
+    per = collections.OrderedDict()
+    for r in data:
+        per.setdefault(r[idi], {})[r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+    ids = list(per)[-k:]
+    out = []
+    for j, i in enumerate(ids):
+        m = per[i]
+        out.append({"launch": j, "dram_read": m.get("dram__bytes_read.sum"), "dram_write": m.get("dram__bytes_write.sum"),
+                    "lts_bytes": m.get("lts__t_bytes.sum"), "us": m.get("gpu__time_duration.sum")})
+    tot = sum((x["dram_read"] or 0) + (x["dram_write"] or 0) for x in out)
+    return {"source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum over the last {k} "
+                      "k_spmm_wide launches (one config-5 step) of bench.py --steps 2 --warmup 3",
+            "launches": out, "dram_bytes_per_launch": tot / len(out) if out else None}
+
+
 if __name__ == "__main__":
     mode = sys.argv[1]
-    if mode == "launches":
+    if mode == "traffic":
+        print(json.dumps(traffic(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 6), indent=1))
+    elif mode == "launches":
         print(json.dumps(launches(sys.argv[2]), indent=1))
     else:
         print(json.dumps([x for p in sys.argv[2:] for x in report(p)], indent=1))
