@@ -7,21 +7,11 @@
 #include <cstring>
 #include <vector>
 
-#include <cstdlib>
-
 #include "common.cuh"
 
 namespace gsg {
 
 static thread_local char g_err[2048] = "";
-
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("GSG_PDL");
-    return !(e && atoi(e) == 0);
-  }();
-  return on;
-}
 
 void set_error(const char* fmt, ...) {
   va_list ap;

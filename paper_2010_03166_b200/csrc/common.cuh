@@ -110,31 +110,6 @@ struct gsg_subgraph {
 namespace gsg {
 inline void count_launch(gsg_ctx* c, int k = 1) { c->launches += k; }
 
-// ---- programmatic dependent launch (PDL) -------------------------------------------------
-// Every kernel of the path is launched with programmatic stream serialization: its CTAs may be
-// scheduled while the previous kernel on the stream drains, run their independent prologue
-// (barrier init, TMEM allocation, tensor-map prefetch), and block in pdl_wait() -- before their
-// first global-memory access of data another kernel produced or consumes -- until the previous
-// grid has completed and flushed. This removes most of the launch gap between the ~25 dependent
-// kernels of a step (CUDA graphs keep the programmatic edges). GSG_PDL=0 disables it.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-bool pdl_enabled();
-template <typename... KArgs, typename... Args>
-cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
-
 // Brackets the kernels of one API-level launch with events when profiling is on.
 struct ProfScope {
   gsg_ctx* c;

@@ -40,8 +40,6 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(int n, int C, int kind, c
                                                        const int32_t* __restrict__ cls, const uint8_t* __restrict__ ind,
                                                        const float* __restrict__ node_w, float* __restrict__ dS,
                                                        float* __restrict__ partial) {
-  pdl_trigger();
-  pdl_wait();
   __shared__ float wsum[kHeadThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = kHeadThreads / 32;
@@ -97,8 +95,6 @@ __global__ void __launch_bounds__(kHeadThreads) k_head(int n, int C, int kind, c
 // shared-memory tree (deterministic).
 __global__ void __launch_bounds__(1024) k_head_final(int nblocks, int n, const float* __restrict__ partial,
                                                      float* __restrict__ loss) {
-  pdl_trigger();
-  pdl_wait();
   __shared__ double sm[1024];
   double t = 0.0;
   for (int b = threadIdx.x; b < nblocks; b += 1024) t += partial[b];
@@ -125,8 +121,8 @@ int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh,
   const int64_t total = (int64_t)rows * cols4;
   int grid = (int)((total + 255) / 256);
   if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
-  GSG_CUDA(launch(k_mask, grid, 256, 0, ctx->stream, rows, cols4, (const float4*)dH, lddh / 4, (const float4*)H,
-                  ldh / 4, (float4*)dZ, lddz / 4, (uint2*)dZlp, lddzlp / 4));
+  k_mask<<<grid, 256, 0, ctx->stream>>>(rows, cols4, (const float4*)dH, lddh / 4, (const float4*)H, ldh / 4,
+                                        (float4*)dZ, lddz / 4, (uint2*)dZlp, lddzlp / 4);
   count_launch(ctx);
   GSG_CUDA(cudaGetLastError());
   return GSG_OK;
@@ -138,10 +134,11 @@ int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64
   if (rc) return rc;
   float* part = (float*)ctx->ws_loss.ptr;
   ProfScope ps(ctx, GSG_K_OTHER, 9.0 * n * C, 0.0);
-  GSG_CUDA(launch(k_head, kHeadBlocks, kHeadThreads, 0, ctx->stream, n, C, kind, S, lds,
-                  kind == GSG_HEAD_SOFTMAX ? (const int32_t*)labels : nullptr,
-                  kind == GSG_HEAD_SIGMOID ? (const uint8_t*)labels : nullptr, node_w, dS, part));
-  GSG_CUDA(launch(k_head_final, 1, 1024, 0, ctx->stream, (int)kHeadBlocks, n, (const float*)part, loss));
+  k_head<<<kHeadBlocks, kHeadThreads, 0, ctx->stream>>>(n, C, kind, S, lds,
+                                                        kind == GSG_HEAD_SOFTMAX ? (const int32_t*)labels : nullptr,
+                                                        kind == GSG_HEAD_SIGMOID ? (const uint8_t*)labels : nullptr,
+                                                        node_w, dS, part);
+  k_head_final<<<1, 1024, 0, ctx->stream>>>(kHeadBlocks, n, part, loss);
   count_launch(ctx, 2);
   GSG_CUDA(cudaGetLastError());
   return GSG_OK;

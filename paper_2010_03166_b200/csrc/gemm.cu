@@ -226,7 +226,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* auxbar = tempty + 2;  // [kEpiWarps] one per epilogue warp: TMA loads of the gate operand
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(auxbar + kEpiWarps);
 
-  pdl_trigger();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int tiles = g.num_m * g.num_n * g.splits;
@@ -262,9 +261,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // PDL: everything above touched only this CTA's smem / TMEM and the kernel parameters; wait
-  // for the previous kernel on the stream before the first global read (TMA) or write
-  pdl_wait();
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs of a pair) =====================
@@ -589,8 +585,6 @@ __device__ __forceinline__ void reduce_store4(const GemmArgs& g, int row, int c,
 // C = epi(sum_s ws[s]) in a fixed split order (deterministic split-K reduction), one thread per
 // output float4 (few splits, many outputs).
 __global__ void k_splitk_reduce(GemmArgs g) {
-  pdl_trigger();
-  pdl_wait();
   const int n4 = (g.N + 3) / 4;
   const int64_t total = (int64_t)g.M * n4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -625,8 +619,6 @@ __global__ void k_splitk_reduce(GemmArgs g) {
 // gradient over K = n cut into 64 pieces): lane l sums splits l, l + 32, ... in order, then a
 // fixed xor-butterfly combines the lanes (deterministic; a different but fixed association).
 __global__ void k_splitk_reduce_warp(GemmArgs g) {
-  pdl_trigger();
-  pdl_wait();
   const int n4 = (g.N + 3) / 4;
   const int64_t total = (int64_t)g.M * n4;
   const int lane = threadIdx.x & 31;
@@ -651,8 +643,6 @@ __global__ void k_splitk_reduce_warp(GemmArgs g) {
 
 // K = 0: C = epi(0) (+ C when accumulating)
 __global__ void k_fill_epi(GemmArgs g) {
-  pdl_trigger();
-  pdl_wait();
   const int64_t total = (int64_t)g.M * g.N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int row = (int)(i / g.N), c = (int)(i % g.N);
@@ -666,8 +656,6 @@ __global__ void k_fill_epi(GemmArgs g) {
 
 __global__ void k_to_bf16(int rows, int cols, const float* __restrict__ src, int64_t lds, __nv_bfloat16* __restrict__ dst,
                           int64_t ldd) {
-  pdl_trigger();
-  pdl_wait();
   const int64_t total = (int64_t)rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / cols), c = (int)(i % cols);
@@ -678,8 +666,6 @@ __global__ void k_to_bf16(int rows, int cols, const float* __restrict__ src, int
 // 4 columns per thread (float4 in, 4 x bf16 = 8 bytes out): cols, lds, ldd multiples of 4.
 __global__ void k_to_bf16_v4(int rows, int cols4, const float4* __restrict__ src, int64_t lds4, uint2* __restrict__ dst,
                              int64_t ldd4) {
-  pdl_trigger();
-  pdl_wait();
   const int64_t total = (int64_t)rows * cols4;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / cols4), c = (int)(i % cols4);
@@ -768,15 +754,13 @@ int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const C
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = ctx->stream;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CTA2 ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cfg.numAttrs = 1;
   GSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, g));
   count_launch(ctx);
   return GSG_OK;
@@ -817,7 +801,7 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   g.Clp = reinterpret_cast<__nv_bfloat16*>(Clp); g.ldclp = ldclp;
   g.aux = aux; g.ldaux = ldaux; g.epi = epilogue; g.accumulate = accumulate;
   if (K == 0) {
-    GSG_CUDA(launch(k_fill_epi, ctx->num_sms * 4, 256, 0, ctx->stream, g));
+    k_fill_epi<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(g);
     count_launch(ctx);
     GSG_CUDA(cudaGetLastError());
     return GSG_OK;
@@ -915,11 +899,11 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
     if (g.splits >= 16 && total < (int64_t)ctx->num_sms * 256) {
       int64_t grid = (total * 32 + 255) / 256;  // one warp per output float4
       if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
-      GSG_CUDA(launch(k_splitk_reduce_warp, (int)grid, 256, 0, ctx->stream, g));
+      k_splitk_reduce_warp<<<(int)grid, 256, 0, ctx->stream>>>(g);
     } else {
       int grid = (int)((total + 255) / 256);
       if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
-      GSG_CUDA(launch(k_splitk_reduce, grid, 256, 0, ctx->stream, g));
+      k_splitk_reduce<<<grid, 256, 0, ctx->stream>>>(g);
     }
     count_launch(ctx);
     GSG_CUDA(cudaGetLastError());
@@ -935,8 +919,8 @@ int to_bf16_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t l
     const int64_t total = (int64_t)rows * (cols / 4);
     int grid = (int)((total + 255) / 256);
     if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
-    GSG_CUDA(launch(k_to_bf16_v4, grid, 256, 0, ctx->stream, rows, cols / 4, reinterpret_cast<const float4*>(src),
-                    lds / 4, static_cast<uint2*>(dst), ldd / 4));
+    k_to_bf16_v4<<<grid, 256, 0, ctx->stream>>>(rows, cols / 4, reinterpret_cast<const float4*>(src), lds / 4,
+                                                static_cast<uint2*>(dst), ldd / 4);
     count_launch(ctx);
     GSG_CUDA(cudaGetLastError());
     return GSG_OK;
@@ -944,7 +928,7 @@ int to_bf16_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t l
   int64_t total = (int64_t)rows * cols;
   int grid = (int)((total + 255) / 256);
   if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
-  GSG_CUDA(launch(k_to_bf16, grid, 256, 0, ctx->stream, rows, cols, src, lds, static_cast<__nv_bfloat16*>(dst), ldd));
+  k_to_bf16<<<grid, 256, 0, ctx->stream>>>(rows, cols, src, lds, static_cast<__nv_bfloat16*>(dst), ldd);
   count_launch(ctx);
   GSG_CUDA(cudaGetLastError());
   return GSG_OK;

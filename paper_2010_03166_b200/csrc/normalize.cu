@@ -18,8 +18,6 @@ __global__ void k_rows(int n, const int64_t* __restrict__ indptr, const int32_t*
                        int mode, int32_t* __restrict__ rowptr, float* __restrict__ rowval,
                        int32_t* __restrict__ counters, int32_t* __restrict__ rowid, int32_t* __restrict__ col,
                        float* __restrict__ val, float* __restrict__ valT) {
-  pdl_trigger();
-  pdl_wait();
   __shared__ int hist[kBins];
   __shared__ int mx;
   if (threadIdx.x < kBins) hist[threadIdx.x] = 0;
@@ -79,8 +77,6 @@ __global__ void k_fill(int64_t nnz, const int64_t* __restrict__ indptr, const in
                        const float* __restrict__ values, int mode, const int32_t* __restrict__ rowid,
                        const float* __restrict__ rowval, int32_t* __restrict__ col, float* __restrict__ val,
                        float* __restrict__ valT) {
-  pdl_trigger();
-  pdl_wait();
   const int self = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_SYM_SELF);
   const bool by_row = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_ROW);
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
@@ -106,8 +102,6 @@ __global__ void k_fill(int64_t nnz, const int64_t* __restrict__ indptr, const in
 // permutation of val).
 __global__ void k_transpose_vals(int n, const int32_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                  const float* __restrict__ val, float* __restrict__ valT, int32_t* __restrict__ err) {
-  pdl_trigger();
-  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
@@ -135,8 +129,6 @@ __global__ void k_transpose_vals(int n, const int32_t* __restrict__ rowptr, cons
 // immaterial: every row is summed by one warp or CTA in CSR order).
 __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t* __restrict__ counters,
                               int32_t* __restrict__ perm) {
-  pdl_trigger();
-  pdl_wait();
   __shared__ int cnt[kBins], base[kBins], off[kBins];
   if (threadIdx.x == 0) {
     int acc = 0, heavy = 0;
@@ -198,24 +190,22 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   int wgrid = (int)(((int64_t)n * 32 + T - 1) / T);
   if (wgrid > ctx->num_sms * 16) wgrid = ctx->num_sms * 16;
   if (wgrid < 1) wgrid = 1;
-  GSG_CUDA(launch(k_rows, wgrid, T, 0, st, n, (const int64_t*)sg->indptr, (const int32_t*)sg->indices, self, mode,
-                  sg->rowptr, sg->rowval, sg->counters, sg->rowid, sg->col, sg->val, sg->valT));
+  k_rows<<<wgrid, T, 0, st>>>(n, sg->indptr, sg->indices, self, mode, sg->rowptr, sg->rowval, sg->counters, sg->rowid,
+                               sg->col, sg->val, sg->valT);
   count_launch(ctx);
   if (n > 0) {
     if (sg->nnz > 0) {
       int64_t eg = (sg->nnz + T - 1) / T;
       if (eg > (int64_t)ctx->num_sms * 16) eg = (int64_t)ctx->num_sms * 16;
-      GSG_CUDA(launch(k_fill, (int)eg, T, 0, st, sg->nnz, (const int64_t*)sg->indptr, (const int32_t*)sg->indices,
-                      (const float*)(sg->has_values ? sg->values : nullptr), mode, (const int32_t*)sg->rowid,
-                      (const float*)sg->rowval, sg->col, sg->val, sg->valT));
+      k_fill<<<(int)eg, T, 0, st>>>(sg->nnz, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode,
+                                    sg->rowid, sg->rowval, sg->col, sg->val, sg->valT);
       count_launch(ctx);
     }
     if (mode == GSG_NORM_VALUES) {
-      GSG_CUDA(launch(k_transpose_vals, wgrid, T, 0, st, n, (const int32_t*)sg->rowptr, (const int32_t*)sg->col,
-                      (const float*)sg->val, sg->valT, sg->counters + 3 * kBins + 4));
+      k_transpose_vals<<<wgrid, T, 0, st>>>(n, sg->rowptr, sg->col, sg->val, sg->valT, sg->counters + 3 * kBins + 4);
       count_launch(ctx);
     }
-    GSG_CUDA(launch(k_bin_scatter, grid, T, 0, st, n, (const int32_t*)sg->rowptr, sg->counters, sg->perm));
+    k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm);
     count_launch(ctx);
   }
   GSG_CUDA(cudaGetLastError());

@@ -251,8 +251,6 @@ __device__ __forceinline__ float4 acc_part(const Acc& A, int q) {
 
 // Full-warp kernel (f > 64): chunk = up to 64 float4 (256 columns), lane owns c4 and c4 + 32.
 __global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
-  pdl_trigger();
-  pdl_wait();
   __shared__ __align__(16) int2 stage[kWarps][32];
   __shared__ float4 part[kWarps][32 * V];
   const int lane = threadIdx.x & 31;
@@ -334,8 +332,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
 // Sub-warp kernel (f <= 64): groups of G lanes, one row per group; heavy rows CTA-split.
 template <int G>
 __global__ void __launch_bounds__(kThreads) k_spmm_narrow(SpmmArgs a) {
-  pdl_trigger();
-  pdl_wait();
   __shared__ float4 part[kWarps][32];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -383,7 +379,7 @@ int launch_k(gsg_ctx* ctx, K kern, int* occ_cache, const SpmmArgs& a, int64_t wa
   int64_t grid = (int64_t)ctx->num_sms * *occ_cache;
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
-  GSG_CUDA(launch(kern, (int)grid, kThreads, 0, ctx->stream, a));
+  kern<<<(int)grid, kThreads, 0, ctx->stream>>>(a);
   count_launch(ctx);
   GSG_CUDA(cudaGetLastError());
   return GSG_OK;
