@@ -334,6 +334,44 @@ def test_layer_stage_isolated(ctx, prec):
     assert rel_err(out["dX"], np.where(Hb > 0, orc.spmm_t(A, T), 0)) <= GEMM_TOL    # a7 after a TF32 GEMM
 
 
+@pytest.mark.parametrize("order2", [False, True])
+def test_layer_w_bf16_flag(ctx, order2):
+    """GSG_W_BF16: a caller-owned bf16 copy of W (made once, shared by forward and backward) gives
+    bit-identical results to the per-call conversion, in both chain orders."""
+    g = graph(4000, 12.0, 900, 80, 21)
+    fi, fo = (96, 64) if order2 else (64, 96)
+    rng = np.random.default_rng(22)
+    X = rng.standard_normal((g.n, fi)).astype(np.float32)
+    W = (rng.standard_normal((fi, fo)) * 0.1).astype(np.float32)
+    dH = rng.standard_normal((g.n, fo)).astype(np.float32)
+    Hb = rng.standard_normal((g.n, fi)).astype(np.float32)
+    sg = ctx.upload(g.indptr, g.indices).normalize()
+    Xd, Wd, dHd, Hbd = dev(X), dev(W), dev(dH), dev(Hb)
+    Wl = torch.zeros((fi, wl.ld_for(fo, 8)), dtype=torch.bfloat16, device="cuda")[:, :fo]
+    ctx.to_bf16(Wd, Wl)
+    f2 = gsg.GSG_ORDER_A_XW if order2 else 0
+    outs = []
+    for Wop, fl in ((Wd, 0), (Wl, gsg.GSG_W_BF16)):
+        P = empty(g.n, fo if order2 else fi)
+        H = empty(g.n, fo)
+        Plp = torch.zeros((g.n, wl.ld_for(fi, 8)), dtype=torch.bfloat16, device="cuda")[:, :fi]
+        ctx.layer_forward(sg, Xd, Wop, P, H, fi, fo, precision=gsg.GSG_PREC_BF16, Plp=None if order2 else Plp,
+                          flags=f2 | fl)
+        if order2:
+            ctx.to_bf16(Xd, Plp)
+        dW, dX = empty(fi, fo), empty(g.n, fi)
+        ctx.layer_backward(sg, Xd if order2 else P, H, dHd, Wop, dW, dX, fi, fo, precision=gsg.GSG_PREC_BF16,
+                           Plp=Plp, H_below=Hbd, flags=f2 | fl)
+        outs.append([host(t) for t in (H, dW, dX)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    with pytest.raises(gsg.GsgError) as e:      # bf16 W with a misaligned stride is refused
+        bad = torch.zeros((fi, fo + 3), dtype=torch.bfloat16, device="cuda")[:, :fo]
+        ctx.layer_forward(sg, Xd, bad, empty(g.n, fi), empty(g.n, fo), fi, fo, precision=gsg.GSG_PREC_BF16,
+                          Plp=Plp, flags=gsg.GSG_W_BF16)
+    assert e.value.code == gsg.GSG_EINVAL
+
+
 def test_layer_end_to_end_config1(ctx):
     cfg = wl.CONFIGS[1]
     g = wl.sample_subgraph(cfg)
