@@ -203,6 +203,7 @@ GSG_API int gsg_ctx_destroy(gsg_ctx_t c) {
   cudaStreamSynchronize(c->stream);
   c->ws_splitk.release(); c->ws_T.release(); c->ws_dZ.release();
   c->ws_lp0.release(); c->ws_lp1.release(); c->ws_lp2.release(); c->ws_loss.release();
+  c->ws_mega.release(); c->ws_megactr.release();
   for (auto& r : c->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->prof.free_ev) cudaEventDestroy(e);
   delete c;

@@ -11,7 +11,10 @@
 namespace gsg {
 
 constexpr int kHeavyMinDeg = 256;   // deg' >= this -> CTA-cooperative row (degree bin "heavy")
+constexpr int kMegaMinDeg = 2048;   // deg' >= this -> the row is split over kMegaSegs CTAs ("mega")
+constexpr int kMegaSegs = 8;
 constexpr int kBins = 32;           // log2 degree buckets
+constexpr int kNMega = 3 * kBins + 6;  // counters[]: number of mega rows (the first ones in perm)
 
 void set_error(const char* fmt, ...);
 int fail(int code, const char* fmt, ...);
@@ -79,6 +82,8 @@ struct gsg_ctx {
   gsg::DevBuf ws_lp1;      // bf16 scratch (dZ copy / T copy)
   gsg::DevBuf ws_lp2;      // bf16 scratch
   gsg::DevBuf ws_loss;     // per-block loss partials
+  gsg::DevBuf ws_mega;     // SpMM mega-row segment partials
+  gsg::DevBuf ws_megactr;  // SpMM mega-row (row, chunk) arrival counters, zero between launches
 };
 
 struct gsg_subgraph {

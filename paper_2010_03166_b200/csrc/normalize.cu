@@ -131,14 +131,18 @@ __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t
                               int32_t* __restrict__ perm) {
   __shared__ int cnt[kBins], base[kBins], off[kBins];
   if (threadIdx.x == 0) {
-    int acc = 0, heavy = 0;
-    const int hb = 32 - __clz(kHeavyMinDeg);
+    int acc = 0, heavy = 0, mega = 0;
+    const int hb = 32 - __clz(kHeavyMinDeg), mb = 32 - __clz(kMegaMinDeg);
     for (int b = kBins - 1; b >= 0; b--) {
       off[b] = acc;
       acc += counters[b];
       if (b >= hb) heavy += counters[b];
+      if (b >= mb) mega += counters[b];
     }
-    if (blockIdx.x == 0) counters[kBins] = heavy;
+    if (blockIdx.x == 0) {
+      counters[kBins] = heavy;
+      counters[kNMega] = mega;  // rows with deg' >= kMegaMinDeg lead perm
+    }
   }
   __syncthreads();
   for (int i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {

@@ -24,6 +24,8 @@
 // Every output row is accumulated in a fixed order -> bitwise reproducible.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include <cstdlib>
 
 #include "common.cuh"
@@ -49,6 +51,10 @@ struct SpmmArgs {
   int64_t ldm4;
   const int32_t* __restrict__ perm;
   const int32_t* __restrict__ n_heavy_ptr;
+  const int32_t* __restrict__ n_mega_ptr;
+  float4* __restrict__ mega_ws;   // [mega row][segment][f4] partials (cap_mega rows)
+  int* __restrict__ mega_ctr;     // [mega row][chunk] arrival counters (zero between launches)
+  int cap_mega;                   // mega rows the workspace holds (more are processed whole)
   int w256;                  // 1: lanes gather 32-byte column pairs with 256-bit loads (X 32-B aligned, ldx % 8 == 0)
 };
 
@@ -259,12 +265,33 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
   const int n_light = a.n - n_heavy;
   int2* st = stage[warp];
 
-  // ---- phase 1: heavy rows, one CTA per (row, chunk), neighbors split across 8 warps ----
-  const int64_t H = (int64_t)n_heavy * a.nchunks;
+  // ---- phase 1: heavy rows, one CTA per (row, chunk), neighbors split across 8 warps; the
+  // mega rows (deg' >= kMegaMinDeg, the first n_mega of perm) additionally split over kMegaSegs
+  // CTAs per chunk: each writes its CTA-reduced partial to the workspace and the last of the
+  // row's segments to arrive (per-(row, chunk) counter) sums them in segment order and stores
+  // (deterministic) -- a 4.5K-degree row no longer serializes ~560 neighbors per warp.
+  const int n_mega = min(*a.n_mega_ptr, a.cap_mega);
+  const int64_t HM = (int64_t)n_mega * kMegaSegs * a.nchunks;
+  const int64_t H = HM + (int64_t)(n_heavy - n_mega) * a.nchunks;
   for (int64_t t = blockIdx.x; t < H; t += gridDim.x) {
-    const int chunk = (int)(t / n_heavy);
-    const int row = a.perm[t % n_heavy];
-    const int b = a.rowptr[row], e = a.rowptr[row + 1];
+    int chunk, row, sgi = -1, m = 0;
+    if (t < HM) {
+      chunk = (int)(t / ((int64_t)n_mega * kMegaSegs));
+      const int r = (int)(t % ((int64_t)n_mega * kMegaSegs));
+      m = r / kMegaSegs;
+      sgi = r % kMegaSegs;
+      row = a.perm[m];
+    } else {
+      const int64_t u = t - HM;
+      chunk = (int)(u / (n_heavy - n_mega));
+      row = a.perm[n_mega + (int)(u % (n_heavy - n_mega))];
+    }
+    int b = a.rowptr[row], e = a.rowptr[row + 1];
+    if (sgi >= 0) {  // this CTA's segment of the mega row
+      const int sl = (e - b + kMegaSegs - 1) / kMegaSegs;
+      b = min(e, b + sgi * sl);
+      e = min(e, b + sl);
+    }
     const int seg = (e - b + kWarps - 1) / kWarps;
     const int w0 = min(e, b + warp * seg), w1 = min(e, w0 + seg);
     const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
@@ -287,15 +314,45 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
     part[warp][lane + 32] = acc_part(A, 1);
     __syncthreads();
     if (warp == 0) {
+      float4 s[V];
 #pragma unroll
       for (int q = 0; q < V; q++) {
-        float4 s = part[0][lane + 32 * q];
+        s[q] = part[0][lane + 32 * q];
 #pragma unroll
         for (int w = 1; w < kWarps; w++) {
           const float4 p = part[w][lane + 32 * q];
-          s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
+          s[q].x += p.x; s[q].y += p.y; s[q].z += p.z; s[q].w += p.w;
         }
-        if (q == 0 ? act0 : act1) store_row(a, row, q == 0 ? c4 : c4b, s);
+      }
+      if (sgi < 0) {
+#pragma unroll
+        for (int q = 0; q < V; q++)
+          if (q == 0 ? act0 : act1) store_row(a, row, q == 0 ? c4 : c4b, s[q]);
+      } else {
+        float4* ws = a.mega_ws + ((int64_t)m * kMegaSegs + sgi) * a.f4;
+#pragma unroll
+        for (int q = 0; q < V; q++)
+          if (q == 0 ? act0 : act1) __stcg(ws + (q == 0 ? c4 : c4b), s[q]);
+        __threadfence();
+        __syncwarp();
+        int prev = 0;
+        if (lane == 0) prev = atomicAdd(a.mega_ctr + (int64_t)m * a.nchunks + chunk, 1);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == kMegaSegs - 1) {  // last segment of this (row, chunk): combine in order
+          __threadfence();
+#pragma unroll
+          for (int q = 0; q < V; q++) {
+            const int cq = q == 0 ? c4 : c4b;
+            if (!(q == 0 ? act0 : act1)) continue;
+            float4 tot = __ldcg(a.mega_ws + (int64_t)m * kMegaSegs * a.f4 + cq);
+            for (int g = 1; g < kMegaSegs; g++) {
+              const float4 p = __ldcg(a.mega_ws + ((int64_t)m * kMegaSegs + g) * a.f4 + cq);
+              tot.x += p.x; tot.y += p.y; tot.z += p.z; tot.w += p.w;
+            }
+            store_row(a, row, cq, tot);
+          }
+          if (lane == 0) a.mega_ctr[(int64_t)m * a.nchunks + chunk] = 0;  // ready for the next launch
+        }
       }
     }
     __syncthreads();
@@ -426,9 +483,23 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   a.ldm4 = ldm / 4;
   a.perm = sg->perm;
   a.n_heavy_ptr = sg->counters + kBins;
+  a.n_mega_ptr = sg->counters + kNMega;
   static int occ_wide = -1, occ16 = -1, occ8 = -1, occ4 = -1;
   if (a.f4 > 16) {
     a.nchunks = (a.f4 + 32 * V - 1) / (32 * V);
+    {  // mega-row workspace: at most nnz' / kMegaMinDeg rows can have deg' >= kMegaMinDeg
+      const int cap = (int)std::min<int64_t>(sg->n, sg->nnz_hat / kMegaMinDeg);
+      a.cap_mega = cap;
+      if (cap > 0) {
+        const int nch = a.nchunks;
+        if (int rc = ctx->ws_mega.reserve(sizeof(float4) * (size_t)cap * kMegaSegs * a.f4)) return rc;
+        void* old = ctx->ws_megactr.ptr;
+        if (int rc = ctx->ws_megactr.reserve(sizeof(int) * (size_t)cap * std::max(nch, 16))) return rc;
+        if (ctx->ws_megactr.ptr != old) GSG_CUDA(cudaMemsetAsync(ctx->ws_megactr.ptr, 0, ctx->ws_megactr.bytes, ctx->stream));
+        a.mega_ws = static_cast<float4*>(ctx->ws_mega.ptr);
+        a.mega_ctr = static_cast<int*>(ctx->ws_megactr.ptr);
+      }
+    }
     a.cw = (a.f4 + a.nchunks - 1) / a.nchunks;
     static int w256_env = -1;
     if (w256_env < 0) { const char* ev = getenv("GSG_SPMM_W256"); w256_env = ev ? atoi(ev) : 1; }

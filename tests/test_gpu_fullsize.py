@@ -149,3 +149,42 @@ def test_step_bitwise_reproducible(ctx, cid):
     second = step.H + step.dX + [step.grad_flat, step.loss]
     for a, b in zip(first, second):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("cid", [2, 5])
+def test_graph_replay_matches_eager(cid):
+    """bench.py times CUDA-graph replays of the step on a side stream; the replayed step must give
+    bit-identical activations, gradients and loss to the eager step checked against the oracle
+    above (config 2 covers chain order 2 on layer 1)."""
+    cfg = wl.CONFIGS[cid]
+    g = wl.sample_subgraph(cfg)
+    inp = wl.make_inputs(cfg, g.n)
+    stream = torch.cuda.Stream()
+    c = gsg.Context(0, stream)
+    with torch.cuda.stream(stream):
+        sg = c.upload(g.indptr, g.indices, validate=True)
+        step = GCNStep(c, cfg.dims, g.n, cfg.head, cfg.classes, cfg.precision, weights=inp.Ws, w_mlp=inp.W_mlp)
+        X = torch.zeros((g.n, wl.ld_for(cfg.dims[0])), device="cuda")[:, :cfg.dims[0]]
+        X.copy_(torch.from_numpy(inp.X))
+        labels = None if inp.labels is None else torch.from_numpy(inp.labels).cuda()
+        dH = None
+        if inp.dH is not None:
+            dH = torch.zeros((g.n, wl.ld_for(cfg.dims[-1])), device="cuda")[:, :cfg.dims[-1]]
+            dH.copy_(torch.from_numpy(inp.dH))
+        step.forward_backward(sg, X, labels=labels, dH_top=dH)
+    stream.synchronize()
+    eager = [t.clone() for t in step.H + step.dX] + [step.grad_flat.clone(), step.loss.clone()]
+    for t in step.H + step.dX + [step.grad_flat, step.loss]:
+        t.zero_()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step.forward_backward(sg, X, labels=labels, dH_top=dH)
+    for _ in range(2):
+        with torch.cuda.stream(stream):
+            graph.replay()
+    stream.synchronize()
+    replay = step.H + step.dX + [step.grad_flat, step.loss]
+    for a, b in zip(eager, replay):
+        assert torch.equal(a, b)
+    c.close()

@@ -130,8 +130,10 @@ def test_spmm_forward_and_transpose(ctx, f):
     assert rel_err(host(Yt), orc.spmm_t(A, X)) <= SPMM_TOL
 
 
-def test_spmm_heavy_rows_and_mask(ctx):
-    g = star_plus_random(3000, 2500, 3)  # hub degree 2500 -> CTA-split heavy row
+@pytest.mark.parametrize("n,hub", [(3000, 2500), (12000, 9000)])
+def test_spmm_heavy_rows_and_mask(ctx, n, hub):
+    # hub degree >= 2048: a "mega" row, split over 8 CTAs per column chunk and combined in order
+    g = star_plus_random(n, hub, 3)
     A = orc.normalize(g.indptr, g.indices, orc.NORM_SYM_SELF)
     sg = ctx.upload(g.indptr, g.indices).normalize(gsg.GSG_NORM_SYM_SELF)
     assert sg.info()["n_heavy"] >= 1
@@ -145,6 +147,9 @@ def test_spmm_heavy_rows_and_mask(ctx):
         assert rel_err(host(Y), ref) <= SPMM_TOL
         yl = host(Ylp)
         assert np.array_equal(yl, torch.from_numpy(host(Y).astype(np.float32)).bfloat16().float().numpy())
+        Y2 = empty(g.n, f)
+        ctx.spmm(sg, dev(X), Y2, transpose=True, mask=dev(Hb))
+        assert torch.equal(Y, Y2)  # the segment combine is order-fixed
 
 
 @pytest.mark.parametrize("f", [65, 200, 300, 1024, 1100])
