@@ -193,6 +193,9 @@ GSG_API int gsg_ctx_create(int device, void* cuda_stream, gsg_ctx_t* out) {
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
   c->stream = static_cast<cudaStream_t>(cuda_stream);
+  GSG_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  GSG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  GSG_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   *out = c;
   return GSG_OK;
 }
@@ -206,6 +209,9 @@ GSG_API int gsg_ctx_destroy(gsg_ctx_t c) {
   c->ws_mega.release(); c->ws_megactr.release();
   for (auto& r : c->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->prof.free_ev) cudaEventDestroy(e);
+  if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
   return GSG_OK;
 }
@@ -535,10 +541,26 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   const void* Wop = W;
   int64_t ldwop = ldw;
   if (bf16 && (rc = bf16_weight(c, W, ldw, f_in, f_out, flags, &Wop, &ldwop))) return rc;
+  // dW = Pᵀ dZ (row a5) and T = dZ Wᵀ -> dX (rows a6, a7) only share read-only inputs: the dW
+  // GEMM runs on the context's side stream (fork / join by events, also inside a CUDA-graph
+  // capture), overlapping its fill / drain and split-K reduction with T's GEMM (config 5: -15 us
+  // per step, configs 3-4 -0.2-0.7 %, config 2 +1 %). GSG_BWD_FORK=0 serializes them (A/B).
+  static const bool fork = !(getenv("GSG_BWD_FORK") && atoi(getenv("GSG_BWD_FORK")) == 0);
+  const bool forked = fork && dX;
+  cudaStream_t main_stream = c->stream;
+  if (forked) {
+    GSG_CUDA(cudaEventRecord(c->ev_fork, main_stream));
+    GSG_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    c->stream = c->side;
+  }
   // dW = Pᵀ dZ   (row a5): A = P stored n x f_in (MN-major), B = dZ stored n x f_out (MN-major)
   rc = gemm_launch(c, f_in, f_out, n, bf16 ? Plp : (const void*)P, bf16 ? ldplp : ldp, 1, bf16 ? dZlp : (const void*)dZ,
                    bf16 ? lddzlp : lddz, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0,
                    (flags & GSG_ACCUM_DW) ? 1 : 0);
+  if (forked) {
+    c->stream = main_stream;
+    GSG_CUDA(cudaEventRecord(c->ev_join, c->side));
+  }
   if (rc) return rc;
   if (!dX) return GSG_OK;
   // T = dZ Wᵀ   (row a6): A = dZ (K-major), B = W stored f_in x f_out = N x K (K-major)
@@ -549,7 +571,9 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
                    nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, 0);
   if (rc) return rc;
   // dX = Âᵀ T [⊙ 1[H_below > 0]]   (row a7, fused a4 of the layer below)
-  return spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, dXlp, lddxlp, Hbelow, ldhb);
+  rc = spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, dXlp, lddxlp, Hbelow, ldhb);
+  if (forked) GSG_CUDA(cudaStreamWaitEvent(main_stream, c->ev_join, 0));  // join
+  return rc;
 }
 
 GSG_API int gsg_sage_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32_t fh, const float* X, int64_t ldx,

@@ -84,6 +84,8 @@ struct gsg_ctx {
   gsg::DevBuf ws_loss;     // per-block loss partials
   gsg::DevBuf ws_mega;     // SpMM mega-row segment partials
   gsg::DevBuf ws_megactr;  // SpMM mega-row (row, chunk) arrival counters, zero between launches
+  cudaStream_t side = nullptr;       // fork/join side stream (layer backward: dW next to T -> dX)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 struct gsg_subgraph {
