@@ -370,16 +370,39 @@ def main():
     step_dist = {"p10": pct(0.1), "p50": pct(0.5), "p90": pct(0.9),
                  "l2": "flushed before every step" if flush is not None else "not flushed (working set vs L2 as in config.l2)"}
 
-    # ---- the same K steps again with CUDA events around every launch (kernel-level rooflines) ----
+    # ---- the same K steps again with CUDA events around every launch (kernel-level rooflines):
+    # captured in one CUDA graph with the event records as graph nodes and replayed once, so the
+    # per-stage times carry no host launch gaps (eager fallback if capture fails) ----
     pv0, pv1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx.profile(True)
-    pv0.record(stream)
-    for i in range(args.steps):
-        step(i)
-    pv1.record(stream)
+    prof_mode = "eager"
+    if graphs is not None:
+        try:
+            pg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(pg, stream=stream):
+                for i in range(args.steps):
+                    step(i, with_comm=False)
+            with torch.cuda.stream(stream):
+                pv0.record(stream)
+                pg.replay()
+                pv1.record(stream)
+            prof_mode = "graph"
+        except Exception:  # noqa: BLE001
+            torch.cuda.synchronize()
+            for k in range(gsg.GSG_K_CLASSES):
+                ctx.profile_read(k)  # drop the partial records of the failed capture
+    if prof_mode == "eager":
+        pv0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        pv1.record(stream)
     stream.synchronize()
     prof = {name: ctx.profile_read(k) for name, k in
             (("spmm", gsg.GSG_K_SPMM), ("gemm", gsg.GSG_K_GEMM), ("normalize", gsg.GSG_K_NORM), ("other", gsg.GSG_K_OTHER))}
+    row_names = (("a1_normalize", gsg.GSG_K_A1), ("a2_aggregate", gsg.GSG_K_A2), ("a3_transform", gsg.GSG_K_A3),
+                 ("a4_gate", gsg.GSG_K_A4), ("a5_dW", gsg.GSG_K_A5), ("a6_T", gsg.GSG_K_A6),
+                 ("a7_aggregate_T", gsg.GSG_K_A7), ("a8_head", gsg.GSG_K_A8))
+    rows_prof = {name: ctx.profile_read(k) for name, k in row_names}
     ctx.profile(False)
     prof_ms = pv0.elapsed_time(pv1)
 
@@ -472,7 +495,8 @@ def main():
                 "kernel": "k_spmm (a2 P=ÂX and a7 dX=ÂᵀT), algorithmic effective gather bytes",
                 "peak_source": peaks["source"], "launches": sp["launches"], "kernel_ms": sp["ms"],
                 "share_of_step": sp["ms"] / prof_ms if prof_ms > 0 else None,
-                "timing": "per-launch CUDA events on the launch stream, second pass of the same K steps"}
+                "timing": f"per-launch CUDA events on the launch stream, second ({prof_mode}-replayed) pass of the "
+                          "same K steps"}
     l2path = os.path.join(ROOT, "profiles", "r01_l2bw.json")
     if os.path.exists(l2path):
         with open(l2path) as f:
@@ -532,6 +556,9 @@ def main():
                "roofline": roofline, "gemm": gemm_info, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches, "launch_mode": graph_note, "clocks": clk.summary(),
                "stages_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
+               "rows_ms_per_step": {k: v["ms"] / args.steps for k, v in rows_prof.items()},
+               "stage_timing": f"per-launch CUDA events ({prof_mode} pass of the same steps, dW GEMM not forked "
+                               "while profiling); ms_per_step is the graph-replayed step",
                "step_ms_dist": step_dist,
                "value_noself": value_noself, "subgraphs_per_s": subgraphs_per_s,
                "layer_roofline_frac": layer_roof,

@@ -119,7 +119,13 @@ GSG_API int64_t gsg_ctx_launch_count(gsg_ctx_t ctx);
  * + 4*n*f per launch; GEMM flops 2*M*N*K. Classes: GSG_K_SPMM, GSG_K_GEMM, GSG_K_NORM,
  * GSG_K_OTHER. gsg_ctx_profile_read synchronizes the stream, returns the totals since the
  * last read and resets them. Enabling allocates events lazily (do it outside graph capture). */
-enum { GSG_K_SPMM = 0, GSG_K_GEMM = 1, GSG_K_NORM = 2, GSG_K_OTHER = 3, GSG_K_CLASSES = 4 };
+enum { GSG_K_SPMM = 0, GSG_K_GEMM = 1, GSG_K_NORM = 2, GSG_K_OTHER = 3,
+       /* the same launches again, by SURVEY §8(a) row (set by the layer / head entry points;
+        * direct gsg_spmm / gsg_gemm calls carry no row): a1 normalize, a2 forward aggregation,
+        * a3 forward transform, a4 standalone ReLU' gate, a5 dW, a6 T = dZ Wᵀ, a7 transposed
+        * aggregation, a8 head (GEMMs + loss) */
+       GSG_K_A1 = 4, GSG_K_A2 = 5, GSG_K_A3 = 6, GSG_K_A4 = 7, GSG_K_A5 = 8, GSG_K_A6 = 9,
+       GSG_K_A7 = 10, GSG_K_A8 = 11, GSG_K_CLASSES = 12 };
 GSG_API int gsg_ctx_profile(gsg_ctx_t ctx, int enable);
 GSG_API int gsg_ctx_profile_read(gsg_ctx_t ctx, int kclass, double* total_ms, int64_t* launches,
                                  double* alg_bytes, double* alg_flops);

@@ -250,11 +250,16 @@ GSG_API int gsg_ctx_profile_read(gsg_ctx_t c, int kclass, double* total_ms, int6
   int64_t cnt = 0;
   std::vector<gsg::Profiler::Rec> keep;
   for (auto& r : c->prof.recs) {
-    if (r.cls != kclass) { keep.push_back(r); continue; }
+    if (r.cls != kclass && r.row != kclass) { keep.push_back(r); continue; }
     float t = 0.f;
     GSG_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
     ms += t;
     cnt++;
+    if (--r.pending > 0) {  // the record still owes its time to its other class
+      if (r.cls == kclass) r.cls = -1; else r.row = -1;
+      keep.push_back(r);
+      continue;
+    }
     c->prof.free_ev.push_back(r.a);
     c->prof.free_ev.push_back(r.b);
   }
@@ -359,6 +364,7 @@ GSG_API int gsg_subgraph_normalize(gsg_ctx_t c, gsg_subgraph_t sg, int mode) {
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   DeviceGuard dg(c->device);
+  RowTag rt(c, GSG_K_A1);
   return normalize_launch(c, sg, mode);
 }
 
@@ -444,6 +450,7 @@ GSG_API int gsg_layer_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
   DeviceGuard dg(c->device);
   const int n = sg->n;
   int rc;
+  RowTag rt(c, GSG_K_A3);  // transform (a3); the aggregation calls below switch to a2
   if (flags & GSG_ORDER_A_XW) {
     // chain order 2 (§7.1): Y = X W (into P), H = ReLU(Â Y)
     GSG_CHECK(ldp >= f_out, GSG_EINVAL, "GSG_ORDER_A_XW: P holds Y = X W and needs ldp >= f_out");
@@ -461,10 +468,13 @@ GSG_API int gsg_layer_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
                        0, 0);
     }
     if (rc) return rc;
+    c->prof_row = GSG_K_A2;
     return spmm_launch(c, sg, 0, f_out, P, ldp, H, ldh, Hlp, ldhlp, nullptr, 0, (flags & GSG_NO_RELU) ? 0 : 1);
   }
+  c->prof_row = GSG_K_A2;
   rc = spmm_launch(c, sg, 0, f_in, X, ldx, P, ldp, precision == GSG_PREC_BF16 ? Plp : nullptr, ldplp, nullptr, 0);
   if (rc) return rc;
+  c->prof_row = GSG_K_A3;
   const int epi = (flags & GSG_NO_RELU) ? GSG_EPI_NONE : GSG_EPI_RELU;
   if (precision == GSG_PREC_BF16) {
     const void* Wl = nullptr;
@@ -492,6 +502,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   const int n = sg->n;
   const bool bf16 = precision == GSG_PREC_BF16;
   int rc;
+  RowTag rt(c, GSG_K_A4);
   // dZ = dH ⊙ 1[H > 0]   (row a4)
   const float* dZ = dH;
   int64_t lddz = lddh;
@@ -528,25 +539,30 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
       if ((rc = c->ws_lp2.reserve(sizeof(uint16_t) * n * ldg))) return rc;
       Glp = c->ws_lp2.ptr;
     }
+    c->prof_row = GSG_K_A7;
     if ((rc = spmm_launch(c, sg, 1, f_out, dZ, lddz, G, ldg, Glp, ldg, nullptr, 0))) return rc;
+    c->prof_row = GSG_K_A5;
     const void* Wop2 = W;
     int64_t ldw2 = ldw;
     if (bf16 && (rc = bf16_weight(c, W, ldw, f_in, f_out, flags, &Wop2, &ldw2))) return rc;
     rc = gemm_launch(c, f_in, f_out, n, bf16 ? Plp : (const void*)P, bf16 ? ldplp : ldp, 1, bf16 ? Glp : (const void*)G,
                      ldg, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, (flags & GSG_ACCUM_DW) ? 1 : 0);
     if (rc || !dX) return rc;
+    c->prof_row = GSG_K_A6;
     return gemm_launch(c, n, f_in, f_out, bf16 ? Glp : (const void*)G, ldg, 0, Wop2, ldw2, 1, dX, lddx, dXlp, lddxlp,
                        precision, Hbelow ? GSG_EPI_MASK : GSG_EPI_NONE, Hbelow, ldhb, 0, 0);
   }
   const void* Wop = W;
   int64_t ldwop = ldw;
+  c->prof_row = GSG_K_A6;
   if (bf16 && (rc = bf16_weight(c, W, ldw, f_in, f_out, flags, &Wop, &ldwop))) return rc;
+  c->prof_row = GSG_K_A5;
   // dW = Pᵀ dZ (row a5) and T = dZ Wᵀ -> dX (rows a6, a7) only share read-only inputs: the dW
   // GEMM runs on the context's side stream (fork / join by events, also inside a CUDA-graph
   // capture), overlapping its fill / drain and split-K reduction with T's GEMM (config 5: -15 us
   // per step, configs 3-4 -0.2-0.7 %, config 2 +1 %). GSG_BWD_FORK=0 serializes them (A/B).
   static const bool fork = !(getenv("GSG_BWD_FORK") && atoi(getenv("GSG_BWD_FORK")) == 0);
-  const bool forked = fork && dX;
+  const bool forked = fork && dX && !c->prof.on;  // profiling serializes (clean per-stage events)
   cudaStream_t main_stream = c->stream;
   if (forked) {
     GSG_CUDA(cudaEventRecord(c->ev_fork, main_stream));
@@ -563,6 +579,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   }
   if (rc) return rc;
   if (!dX) return GSG_OK;
+  c->prof_row = GSG_K_A6;
   // T = dZ Wᵀ   (row a6): A = dZ (K-major), B = W stored f_in x f_out = N x K (K-major)
   const int64_t ldt = round_up(f_in, 4);
   if ((rc = c->ws_T.reserve(sizeof(float) * n * ldt))) return rc;
@@ -571,6 +588,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
                    nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, 0);
   if (rc) return rc;
   // dX = Âᵀ T [⊙ 1[H_below > 0]]   (row a7, fused a4 of the layer below)
+  c->prof_row = GSG_K_A7;
   rc = spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, dXlp, lddxlp, Hbelow, ldhb);
   if (forked) GSG_CUDA(cudaStreamWaitEvent(main_stream, c->ev_join, 0));  // join
   return rc;
@@ -650,6 +668,7 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
   GSG_CHECK(lds >= C && lds % 4 == 0, GSG_EINVAL, "lds must be >= C and a multiple of 4");
   (void)precision;  // the head runs in TF32: H_L is fp32 and C is small (SUPPORT)
   DeviceGuard dg(c->device);
+  RowTag rt(c, GSG_K_A8);
   int rc = gemm_launch(c, n, C, f, HL, ldh, 0, Wm, ldw, 0, S, lds, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
   if (rc) return rc;
   if ((rc = head_loss_launch(c, n, C, kind, S, lds, labels, node_w, dS, loss))) return rc;

@@ -55,7 +55,7 @@ namespace gsg {
 // Per-class CUDA-event profiler (gsg_ctx_profile).
 struct Profiler {
   bool on = false;
-  struct Rec { int cls; cudaEvent_t a, b; };
+  struct Rec { int cls, row, pending; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> free_ev;
   double bytes[GSG_K_CLASSES] = {}, flops[GSG_K_CLASSES] = {};
@@ -75,6 +75,7 @@ struct gsg_ctx {
   bool own_stream = false;
   int num_sms = 148;
   int64_t launches = 0;
+  int prof_row = -1;       // SURVEY §8(a) row of the launches being issued (GSG_K_A*), -1 = none
   gsg::DevBuf ws_splitk;   // split-K partials
   gsg::DevBuf ws_T;        // T = dZ Wᵀ (fp32)
   gsg::DevBuf ws_dZ;       // masked dZ (fp32)
@@ -126,15 +127,28 @@ struct ProfScope {
     if (!c->prof.on) return;
     c->prof.bytes[cls] += bytes;
     c->prof.flops[cls] += flops;
+    if (c->prof_row >= 0) {
+      c->prof.bytes[c->prof_row] += bytes;
+      c->prof.flops[c->prof_row] += flops;
+    }
     a = c->prof.get();
-    cudaEventRecord(a, c->stream);
+    // external records stay timing events when the launches are captured into a CUDA graph
+    cudaEventRecordWithFlags(a, c->stream, cudaEventRecordExternal);
   }
   ~ProfScope() {
     if (!a) return;
     cudaEvent_t b = c->prof.get();
-    cudaEventRecord(b, c->stream);
-    c->prof.recs.push_back({cls, a, b});
+    cudaEventRecordWithFlags(b, c->stream, cudaEventRecordExternal);
+    c->prof.recs.push_back({cls, c->prof_row, c->prof_row >= 0 ? 2 : 1, a, b});
   }
+};
+
+// Tags the launches issued in its scope with a SURVEY §8(a) row (GSG_K_A*).
+struct RowTag {
+  gsg_ctx* c;
+  int prev;
+  RowTag(gsg_ctx* c_, int row) : c(c_), prev(c_->prof_row) { c->prof_row = row; }
+  ~RowTag() { c->prof_row = prev; }
 };
 
 // launch wrappers implemented in the .cu files
