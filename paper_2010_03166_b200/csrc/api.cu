@@ -672,9 +672,25 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
   int rc = gemm_launch(c, n, C, f, HL, ldh, 0, Wm, ldw, 0, S, lds, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
   if (rc) return rc;
   if ((rc = head_loss_launch(c, n, C, kind, S, lds, labels, node_w, dS, loss))) return rc;
+  // dW_mlp = H_Lᵀ dS and dH_L = (dS W_mlpᵀ) ⊙ 1[H_L > 0] only share read-only inputs: the first
+  // runs on the side stream (fork / join, as in gsg_layer_backward; serialized while profiling)
+  static const bool fork = !(getenv("GSG_BWD_FORK") && atoi(getenv("GSG_BWD_FORK")) == 0);
+  const bool forked = fork && !c->prof.on;
+  cudaStream_t main_stream = c->stream;
+  if (forked) {
+    GSG_CUDA(cudaEventRecord(c->ev_fork, main_stream));
+    GSG_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    c->stream = c->side;
+  }
   rc = gemm_launch(c, f, C, n, HL, ldh, 1, dS, lds, 0, dWm, lddw, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
+  if (forked) {
+    c->stream = main_stream;
+    GSG_CUDA(cudaEventRecord(c->ev_join, c->side));
+  }
   if (rc) return rc;
-  return gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, GSG_PREC_TF32, GSG_EPI_MASK, HL, ldh, 0, 0);
+  rc = gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, GSG_PREC_TF32, GSG_EPI_MASK, HL, ldh, 0, 0);
+  if (forked) GSG_CUDA(cudaStreamWaitEvent(main_stream, c->ev_join, 0));  // join
+  return rc;
 }
 
 // ------------------------------------------------------------------------------ NCCL
