@@ -34,6 +34,7 @@ GSG_HEAD_SOFTMAX, GSG_HEAD_SIGMOID = 0, 1
 GSG_K_SPMM, GSG_K_GEMM, GSG_K_NORM, GSG_K_OTHER = 0, 1, 2, 3
 # the same launches by SURVEY §8(a) row (gsg.h): a1 normalize ... a8 head
 GSG_K_A1, GSG_K_A2, GSG_K_A3, GSG_K_A4, GSG_K_A5, GSG_K_A6, GSG_K_A7, GSG_K_A8 = range(4, 12)
+GSG_K_CLASSES = 12
 
 _vp, _i32, _i64, _int = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int
 _SIGS = {

@@ -204,7 +204,7 @@ GSG_API int gsg_ctx_destroy(gsg_ctx_t c) {
   if (!c) return GSG_OK;
   DeviceGuard dg(c->device);
   cudaStreamSynchronize(c->stream);
-  c->ws_splitk.release(); c->ws_T.release(); c->ws_dZ.release();
+  c->ws_splitk.release(); c->ws_splitk_side.release(); c->ws_T.release(); c->ws_dZ.release();
   c->ws_lp0.release(); c->ws_lp1.release(); c->ws_lp2.release(); c->ws_loss.release();
   c->ws_mega.release(); c->ws_megactr.release();
   for (auto& r : c->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -570,9 +570,11 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
     c->stream = c->side;
   }
   // dW = Pᵀ dZ   (row a5): A = P stored n x f_in (MN-major), B = dZ stored n x f_out (MN-major)
+  c->side_ws = true;
   rc = gemm_launch(c, f_in, f_out, n, bf16 ? Plp : (const void*)P, bf16 ? ldplp : ldp, 1, bf16 ? dZlp : (const void*)dZ,
                    bf16 ? lddzlp : lddz, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0,
                    (flags & GSG_ACCUM_DW) ? 1 : 0);
+  c->side_ws = false;
   if (forked) {
     c->stream = main_stream;
     GSG_CUDA(cudaEventRecord(c->ev_join, c->side));
@@ -682,7 +684,9 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
     GSG_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     c->stream = c->side;
   }
+  c->side_ws = true;
   rc = gemm_launch(c, f, C, n, HL, ldh, 1, dS, lds, 0, dWm, lddw, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
+  c->side_ws = false;
   if (forked) {
     c->stream = main_stream;
     GSG_CUDA(cudaEventRecord(c->ev_join, c->side));

@@ -76,7 +76,9 @@ struct gsg_ctx {
   int num_sms = 148;
   int64_t launches = 0;
   int prof_row = -1;       // SURVEY §8(a) row of the launches being issued (GSG_K_A*), -1 = none
-  gsg::DevBuf ws_splitk;   // split-K partials
+  gsg::DevBuf ws_splitk;   // split-K partials (context stream)
+  gsg::DevBuf ws_splitk_side;  // split-K partials of the GEMMs that may be forked onto the side stream
+  bool side_ws = false;        // gemm_launch uses ws_splitk_side (set around those GEMMs, forked or not)
   gsg::DevBuf ws_T;        // T = dZ Wᵀ (fp32)
   gsg::DevBuf ws_dZ;       // masked dZ (fp32)
   gsg::DevBuf ws_lp0;      // bf16 scratch (W copy)

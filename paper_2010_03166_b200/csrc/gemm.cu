@@ -853,9 +853,13 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   g.mpad = g.num_m * BMT;
   if (g.splits > 1) {
     g.ldws = (N + 7) / 8 * 8;
-    rc = ctx->ws_splitk.reserve((size_t)g.splits * g.mpad * g.ldws * sizeof(float));
+    // a GEMM forked onto the side stream may run concurrently with one on the context stream:
+    // the forkable GEMMs (dW, dW_mlp) always use their own workspace, forked or not, so that a
+    // serialized (profiling) pass inside a graph capture never has to grow it
+    DevBuf& wsk = ctx->side_ws ? ctx->ws_splitk_side : ctx->ws_splitk;
+    rc = wsk.reserve((size_t)g.splits * g.mpad * g.ldws * sizeof(float));
     if (rc) return rc;
-    g.ws = static_cast<float*>(ctx->ws_splitk.ptr);
+    g.ws = static_cast<float*>(wsk.ptr);
   }
   // instruction descriptor: D=F32, A/B = TF32 (2) or BF16 (1), majorness, N>>3, M>>4
   const uint32_t fmt = bf16 ? 1u : 2u;

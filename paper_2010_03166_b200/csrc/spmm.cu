@@ -51,6 +51,7 @@ struct SpmmArgs {
   int64_t ldm4;
   const int32_t* __restrict__ perm;
   const int32_t* __restrict__ n_heavy_ptr;
+  const int32_t* __restrict__ bucket_counts;  // [kBins] rows per log2 degree bucket
   const int32_t* __restrict__ n_mega_ptr;
   float4* __restrict__ mega_ws;   // [mega row][segment][f4] partials (cap_mega rows)
   int* __restrict__ mega_ctr;     // [mega row][chunk] arrival counters (zero between launches)
@@ -186,37 +187,34 @@ __device__ __forceinline__ void warp_row_sum256(const SpmmArgs& a, int2* __restr
 }
 
 // Sub-warp (group of G lanes, one row) accumulation; no shuffles (groups diverge).
+__device__ __forceinline__ void fma4(float4& acc, float w, const float4& v) {
+  acc.x = fmaf(w, v.x, acc.x);
+  acc.y = fmaf(w, v.y, acc.y);
+  acc.z = fmaf(w, v.z, acc.z);
+  acc.w = fmaf(w, v.w, acc.w);
+}
+
+// 8 neighbors per batch: the 8 (col, val) loads, then the 8 row gathers, are independent, so a
+// row costs one dependent round trip per 8 neighbors; the last batch is predicated.
 __device__ __forceinline__ float4 group_row_sum(const SpmmArgs& a, int b, int e, int c4, bool act) {
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4* Xc = a.X + c4;
-  int k = b;
-  for (; k + 4 <= e; k += 4) {
-    uint32_t c[4];
-    float w[4];
-    float4 v[4];
+  for (int k = b; k < e; k += 8) {
+    uint32_t c[8];
+    float w[8];
+    float4 v[8];
 #pragma unroll
-    for (int u = 0; u < 4; u++) { c[u] = (uint32_t)__ldg(a.col + k + u) * a.ldx4; w[u] = __ldg(a.val + k + u); }
-    if (act) {
-#pragma unroll
-      for (int u = 0; u < 4; u++) v[u] = __ldg(Xc + c[u]);
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        acc.x = fmaf(w[u], v[u].x, acc.x);
-        acc.y = fmaf(w[u], v[u].y, acc.y);
-        acc.z = fmaf(w[u], v[u].z, acc.z);
-        acc.w = fmaf(w[u], v[u].w, acc.w);
-      }
+    for (int u = 0; u < 8; u++) {
+      const bool ok = k + u < e;
+      c[u] = ok ? (uint32_t)__ldg(a.col + k + u) * a.ldx4 : 0u;
+      w[u] = ok ? __ldg(a.val + k + u) : 0.f;
     }
-  }
-  for (; k < e; k++) {
-    const uint32_t c = (uint32_t)__ldg(a.col + k) * a.ldx4;
-    const float w = __ldg(a.val + k);
     if (act) {
-      const float4 v = __ldg(Xc + c);
-      acc.x = fmaf(w, v.x, acc.x);
-      acc.y = fmaf(w, v.y, acc.y);
-      acc.z = fmaf(w, v.z, acc.z);
-      acc.w = fmaf(w, v.w, acc.w);
+#pragma unroll
+      for (int u = 0; u < 8; u++) v[u] = k + u < e ? __ldg(Xc + c[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (k + u < e) fma4(acc, w[u], v[u]);
     }
   }
   return acc;
@@ -387,39 +385,52 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
 }
 
 // Sub-warp kernel (f <= 64): groups of G lanes, one row per group; heavy rows CTA-split.
+// Rows with deg' >= kNarrowSplitDeg (the first rows of the degree-sorted order; at most two per
+// CTA) are split over all NG = 8 * 32/G lane groups of a CTA and reduced through shared memory
+// in group order; every other row is one group's. (At f <= 64 a row costs one dependent round
+// trip per 8 neighbors, so a 170-degree row alone would otherwise set the kernel's length.)
+constexpr int kNarrowSplitDeg = 64;
 template <int G>
 __global__ void __launch_bounds__(kThreads) k_spmm_narrow(SpmmArgs a) {
-  __shared__ float4 part[kWarps][32];
+  constexpr int PER = 32 / G;
+  constexpr int NG = kWarps * PER;
+  __shared__ float4 part[NG][G];
+  __shared__ int s_nh;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int n_heavy = *a.n_heavy_ptr;
-  const int n_light = a.n - n_heavy;
-  for (int64_t t = blockIdx.x; t < n_heavy; t += gridDim.x) {
+  const int g = lane / G, gl = lane % G;
+  const int gi = warp * PER + g;
+  if (threadIdx.x == 0) {  // at most two split rows per CTA: enough to cut the critical path of
+    int h = 0;              // a few outlier rows without serializing a batch's many medium rows
+    for (int bkt = 32 - __clz(kNarrowSplitDeg); bkt < kBins; bkt++) h += a.bucket_counts[bkt];
+    s_nh = min(h, 2 * (int)gridDim.x);
+  }
+  __syncthreads();
+  const int n_split = s_nh;
+  const int n_rest = a.n - n_split;
+  const bool act = gl < a.f4;
+  for (int64_t t = blockIdx.x; t < n_split; t += gridDim.x) {
     const int row = a.perm[t];
     const int b = a.rowptr[row], e = a.rowptr[row + 1];
-    const int seg = (e - b + kWarps - 1) / kWarps;
-    const int w0 = min(e, b + warp * seg), w1 = min(e, w0 + seg);
-    const bool act = lane < a.f4;
-    part[warp][lane] = group_row_sum(a, w0, w1, lane, act);
+    const int seg = (e - b + NG - 1) / NG;
+    const int w0 = min(e, b + gi * seg), w1 = min(e, w0 + seg);
+    part[gi][gl] = group_row_sum(a, w0, w1, gl, act);
     __syncthreads();
-    if (warp == 0) {
-      float4 s = part[0][lane];
-#pragma unroll
-      for (int w = 1; w < kWarps; w++) {
-        const float4 p = part[w][lane];
-        s.x += p.x; s.y += p.y; s.z += p.z; s.w += p.w;
+    if (threadIdx.x < G) {
+      float4 s4 = part[0][threadIdx.x];
+#pragma unroll 4
+      for (int q = 1; q < NG; q++) {
+        const float4 p = part[q][threadIdx.x];
+        s4.x += p.x; s4.y += p.y; s4.z += p.z; s4.w += p.w;
       }
-      if (act) store_row(a, row, lane, s);
+      if ((int)threadIdx.x < a.f4) store_row(a, row, threadIdx.x, s4);
     }
     __syncthreads();
   }
-  constexpr int PER = 32 / G;
-  const int g = lane / G, gl = lane % G;
   const int64_t gid = ((int64_t)blockIdx.x * kWarps + warp) * PER + g;
   const int64_t GN = (int64_t)gridDim.x * kWarps * PER;
-  const bool act = gl < a.f4;
-  for (int64_t t = gid; t < n_light; t += GN) {
-    const int row = a.perm[n_heavy + (int)t];
+  for (int64_t t = gid; t < n_rest; t += GN) {
+    const int row = a.perm[n_split + (int)t];
     const float4 acc = group_row_sum(a, a.rowptr[row], a.rowptr[row + 1], gl, act);
     if (act) store_row(a, row, gl, acc);
   }
@@ -483,6 +494,7 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   a.ldm4 = ldm / 4;
   a.perm = sg->perm;
   a.n_heavy_ptr = sg->counters + kBins;
+  a.bucket_counts = sg->counters;
   a.n_mega_ptr = sg->counters + kNMega;
   static int occ_wide = -1, occ16 = -1, occ8 = -1, occ4 = -1;
   if (a.f4 > 16) {

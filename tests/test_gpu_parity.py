@@ -339,6 +339,23 @@ def test_layer_stage_isolated(ctx, prec):
     assert rel_err(out["dX"], np.where(Hb > 0, orc.spmm_t(A, T), 0)) <= GEMM_TOL    # a7 after a TF32 GEMM
 
 
+def test_layer_backward_concurrent_splitk(ctx):
+    """Shapes where both backward GEMMs cut K (dW: 2 tiles, K = n; T: 8 tiles, K = 512) while
+    dW runs on the side stream next to T -> dX: each stream has its own split-K workspace."""
+    g = graph(4000, 12.0, 1000, 80, 31)
+    fi, fo = 64, 512
+    rng = np.random.default_rng(32)
+    X = rng.standard_normal((g.n, fi)).astype(np.float32)
+    W = (rng.standard_normal((fi, fo)) * 0.05).astype(np.float32)
+    dH = rng.standard_normal((g.n, fo)).astype(np.float32)
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW_SELF)
+    for _ in range(2):
+        out = run_layer(ctx, g, X, W, dH, gsg.GSG_PREC_TF32)
+        dZ = orc.relu_mask(dH, out["H"])
+        assert rel_err(out["dW"], orc.gemm(out["P"], dZ, transA=True)) <= GEMM_TOL
+        assert rel_err(out["dX"], orc.spmm_t(A, orc.gemm(dZ, W, transB=True))) <= GEMM_TOL
+
+
 @pytest.mark.parametrize("order2", [False, True])
 def test_layer_w_bf16_flag(ctx, order2):
     """GSG_W_BF16: a caller-owned bf16 copy of W (made once, shared by forward and backward) gives
