@@ -192,6 +192,85 @@ def run_reference(args, cfg):
     return 0
 
 
+def run_gpu_sampled(args, cfg, ctx, runner, stream, dev, rank):
+    """Training loop fed by the GPU frontier sampler (NEXT #3, Alg. 2 on the device): the parent
+    graph and a seeded parent feature matrix (and labels) live in HBM; every --sampler-pool steps
+    one gsg_frontier_sample call draws that many subgraphs; each step copies its CSR into the
+    step's subgraph (device to device), gathers X_s = X[V_s] and the labels (gsg_gather_rows,
+    Alg. 1 line 5), normalizes and runs the layers eagerly (subgraph sizes vary, so no graph).
+    Returns the loop's edge-features/s including the sampling, and the sampler's share."""
+    import torch
+    import paper_2010_03166_b200 as gsg
+    P = max(1, args.sampler_pool)
+    pc = wl.parent_for(cfg).csr()
+    pg = gsg.ParentGraph(ctx, pc.indptr, pc.indices)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(cfg.seed(2, 0, rank) + 7)
+    f0 = cfg.dims[0]
+    with torch.cuda.stream(stream):
+        Xpar = torch.randn((pc.n, wl.ld_for(f0)), device=dev, generator=gen)[:, :f0]
+        if cfg.head == "softmax":
+            Lpar = torch.randint(0, cfg.classes, (pc.n, 1), device=dev, generator=gen, dtype=torch.int32)
+        elif cfg.head == "sigmoid":
+            Lpar = (torch.rand((pc.n, cfg.classes), device=dev, generator=gen) < cfg.label_p).to(torch.uint8)
+        else:
+            Lpar = None
+        n_max = runner.n_max
+        Xs = torch.zeros((n_max, wl.ld_for(f0)), device=dev)[:, :f0]
+        Ls = None if Lpar is None else torch.zeros((n_max, Lpar.shape[1]), dtype=Lpar.dtype, device=dev)
+        dH = None
+        if cfg.head == "none":
+            dH = torch.randn((n_max, wl.ld_for(cfg.dims[-1])), device=dev, generator=gen)[:, :cfg.dims[-1]]
+    g0 = wl.sample_subgraph(cfg, 0, rank)
+    sgl = ctx.upload(g0.indptr, g0.indices, validate=False)
+    state = {"batch": None, "sample_ms": 0.0}
+    seed0 = cfg.seed(10, 0, rank) + 777
+
+    def gs_step(i):
+        if i % P == 0:
+            if state["batch"] is not None:
+                stream.synchronize()
+                state["batch"].free()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            state["batch"] = pg.sample(cfg.n, cfg.m, seed0 + i, count=P)
+            b.record(stream)
+            state["events"] = (a, b)
+        info = state["batch"].get(i % P)
+        n, nnz = info["n"], info["nnz"]
+        with torch.cuda.stream(stream):
+            sgl.assign(n, nnz, info["d_indptr"], info["d_indices"])
+            ctx.gather_rows(Xpar, info["d_nodes"], Xs, n)
+            if Ls is not None:
+                ctx.gather_rows(Lpar, info["d_nodes"], Ls, n)
+            labels = None if Ls is None else (Ls[:n, 0] if cfg.head == "softmax" else Ls[:n])
+            runner.forward_backward(sgl, Xs[:n], labels=labels, dH_top=None if dH is None else dH[:n])
+        return runner.work_edge_features(nnz + n)
+
+    for i in range(P):  # warm-up: one full pool
+        gs_step(i)
+    stream.synchronize()
+    steps = 2 * P
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    work, samp_ms = 0, 0.0
+    e0.record(stream)
+    for i in range(P, P + steps):
+        work += gs_step(i)
+        if i % P == 0:
+            stream.synchronize()
+            samp_ms += state["events"][0].elapsed_time(state["events"][1])
+    e1.record(stream)
+    stream.synchronize()
+    ms = e0.elapsed_time(e1)
+    state["batch"].free()
+    pg.free()
+    return {"value": work / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+            "subgraphs_per_gpu_sampler_call": P, "sampler_ms_per_subgraph": samp_ms / steps,
+            "sampler_share": samp_ms / ms,
+            "note": "fresh GPU-sampled subgraph every step (eager launches), features / labels gathered from "
+                    "parent arrays in HBM; includes the sampling kernels"}
+
+
 # ------------------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -208,6 +287,11 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
     ap.add_argument("--batch", type=int, default=1,
                     help="B independent subgraphs per step as one block-diagonal graph (SURVEY §8(d) batched variant)")
+    ap.add_argument("--sampler", default="host", choices=["host", "gpu"],
+                    help="gpu: additionally time a training loop whose subgraphs are frontier-sampled on the GPU "
+                         "(NEXT #3) from a device-resident parent graph, features gathered from a parent feature "
+                         "matrix in HBM, a fresh subgraph every step")
+    ap.add_argument("--sampler-pool", type=int, default=64, help="subgraphs per GPU sampling call (--sampler gpu)")
     ap.add_argument("--flush-l2", action="store_true",
                     help="flush L2 (write a 2x-L2 buffer) before every step of the per-step timing pass")
     args = ap.parse_args()
@@ -541,6 +625,11 @@ def main():
                "sample": f"rows [0,{osamp.rows}) of the first subgraph, all {cfg.L} layers fwd+bwd + head, "
                          f"fp64 plain loops, {dt_:.1f} s"}
 
+    # ---- optional: the same step fed by the GPU sampler (a fresh subgraph every step) ----
+    gpu_loop = None
+    if args.sampler == "gpu" and args.batch == 1:
+        gpu_loop = run_gpu_sampled(args, cfg, ctx, runner, stream, dev, rank)
+
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
@@ -563,6 +652,8 @@ def main():
                "value_noself": value_noself, "subgraphs_per_s": subgraphs_per_s,
                "layer_roofline_frac": layer_roof,
                "setup_s": time.time() - t_setup}
+        if gpu_loop is not None:
+            out["gpu_sampled_loop"] = gpu_loop
         print(json.dumps(out), flush=True)
     if comm is not None:
         stream.synchronize()

@@ -150,9 +150,12 @@ GSG_API const char* gsg_last_error(void);
 GSG_API int gsg_subgraph_upload(gsg_ctx_t ctx, int32_t n, int64_t nnz, const int64_t* h_indptr,
                                 const int32_t* h_indices, const float* h_values, int validate,
                                 gsg_subgraph_t* out);
-/* Refill an existing subgraph with a new host CSR (same contract as gsg_subgraph_upload),
+/* Refill an existing subgraph with a new CSR (same contract as gsg_subgraph_upload),
  * reusing its device arrays when they are large enough (no allocation in the steady state;
- * copies are asynchronous from pinned host memory). The subgraph must be normalized again. */
+ * copies are asynchronous from pinned host memory). The arrays may also be DEVICE-resident,
+ * e.g. a GPU-sampled subgraph from gsg_sample_get (device-to-device copy; validate must be 0
+ * and nnz must match indptr[n], which the library cannot check without a synchronization).
+ * The subgraph must be normalized again. */
 GSG_API int gsg_subgraph_assign(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t n, int64_t nnz,
                                 const int64_t* h_indptr, const int32_t* h_indices,
                                 const float* h_values, int validate);
@@ -325,6 +328,13 @@ GSG_API int gsg_sample_get(gsg_sample_t s, int32_t k, int32_t* n_k, int64_t* nnz
                            const int64_t** d_indptr, const int32_t** d_indices,
                            const int32_t** d_nodes);
 GSG_API int gsg_sample_free(gsg_sample_t s);
+/* Row gather for the sampled subgraph's inputs (Alg. 1 line 5: X_s = X[V_s], the labels
+ * likewise): dst row r (row_bytes bytes, pitch dst_pitch) = src row d_idx[r] (pitch src_pitch),
+ * r < rows, all DEVICE pointers (e.g. d_nodes of gsg_sample_get into a parent feature matrix
+ * resident in HBM). 16-byte vectors when all pointers, pitches and row_bytes are 16-byte
+ * multiples. Errors: GSG_EINVAL (negative sizes, NULL, pitch < row_bytes). */
+GSG_API int gsg_gather_rows(gsg_ctx_t ctx, int32_t rows, int64_t row_bytes, const void* d_src,
+                            int64_t src_pitch, const int32_t* d_idx, void* d_dst, int64_t dst_pitch);
 
 /* ==== data parallelism (row a9) ======================================================== */
 /* NCCL plumbing (libnccl.so.2 is resolved at run time; the process's already-loaded copy,

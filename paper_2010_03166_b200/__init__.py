@@ -73,6 +73,7 @@ _SIGS = {
     "gsg_parent_upload": (_int, [_vp, _i64, _i64, _vp, _vp, ctypes.POINTER(_vp)]),
     "gsg_parent_free": (_int, [_vp]),
     "gsg_frontier_sample": (_int, [_vp, _vp, _i32, _i32, _i32, ctypes.c_uint64, _i32, ctypes.POINTER(_vp)]),
+    "gsg_gather_rows": (_int, [_vp, _i32, _i64, _vp, _i64, _vp, _vp, _i64]),
     "gsg_sample_get": (_int, [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
     "gsg_sample_free": (_int, [_vp]),
@@ -320,6 +321,14 @@ class Context:
         return Subgraph(self, out.value, n, nnz)
 
     # ---- kernels ----
+    def gather_rows(self, src, idx_ptr: int, dst, rows: int):
+        """dst[r, :] = src[idx[r], :] for r < rows (2-D row-major device tensors of one dtype;
+        idx_ptr: device int32 array, e.g. the d_nodes of a GPU sample)."""
+        es = src.element_size()
+        assert dst.element_size() == es and src.shape[1] == dst.shape[1]
+        check(gsg_gather_rows(self.h, rows, src.shape[1] * es, _ptr(src), src.stride(0) * es, idx_ptr, _ptr(dst),
+                              dst.stride(0) * es))
+
     def spmm(self, sg: Subgraph, X, Y, transpose: bool = False, Ylp=None, mask=None, f: int | None = None):
         f = X.shape[1] if f is None else f
         check(gsg_spmm(self.h, sg.h, int(transpose), f, _ptr(X), _ld(X), _ptr(Y), _ld(Y), _ptr(Ylp) or None, _ld(Ylp),

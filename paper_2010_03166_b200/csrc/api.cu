@@ -308,7 +308,12 @@ GSG_API int gsg_subgraph_assign(gsg_ctx_t c, gsg_subgraph_t sg, int32_t n, int64
   GSG_CHECK(n >= 0 && nnz >= 0, GSG_EINVAL, "negative n (%d) or nnz (%lld)", n, (long long)nnz);
   GSG_CHECK(h_indptr && (nnz == 0 || h_indices), GSG_EINVAL, "NULL indptr/indices");
   GSG_CHECK(nnz + (int64_t)n < (int64_t)INT32_MAX, GSG_EUNSUPPORTED, "nnz + n exceeds int32 indexing");
-  if (validate) {
+  cudaPointerAttributes pa{};
+  const bool on_device = cudaPointerGetAttributes(&pa, h_indptr) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+  cudaGetLastError();  // clear a pointer-query error for plain (unregistered) host memory
+  if (on_device) {
+    GSG_CHECK(!validate, GSG_EINVAL, "validate needs host arrays (the CSR is device-resident)");
+  } else if (validate) {
     if (int rc = validate_csr(n, nnz, h_indptr, h_indices)) return rc;
   } else {
     GSG_CHECK(h_indptr[n] == nnz, GSG_EGRAPH, "indptr[n] = %lld != nnz = %lld", (long long)h_indptr[n], (long long)nnz);
@@ -334,11 +339,19 @@ GSG_API int gsg_subgraph_assign(gsg_ctx_t c, gsg_subgraph_t sg, int32_t n, int64
   sg->nnz = nnz;
   sg->norm_mode = -1;
   sg->has_values = h_values != nullptr;
-  GSG_CUDA(cudaMemcpyAsync(sg->indptr, h_indptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, c->stream));
-  if (nnz) GSG_CUDA(cudaMemcpyAsync(sg->indices, h_indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c->stream));
+  // cudaMemcpyDefault: host (pinned or pageable) or device source arrays (UVA)
+  GSG_CUDA(cudaMemcpyAsync(sg->indptr, h_indptr, sizeof(int64_t) * (n + 1), cudaMemcpyDefault, c->stream));
+  if (nnz) GSG_CUDA(cudaMemcpyAsync(sg->indices, h_indices, sizeof(int32_t) * nnz, cudaMemcpyDefault, c->stream));
   if (h_values && nnz)
-    GSG_CUDA(cudaMemcpyAsync(sg->values, h_values, sizeof(float) * nnz, cudaMemcpyHostToDevice, c->stream));
+    GSG_CUDA(cudaMemcpyAsync(sg->values, h_values, sizeof(float) * nnz, cudaMemcpyDefault, c->stream));
   return GSG_OK;
+}
+
+GSG_API int gsg_gather_rows(gsg_ctx_t c, int32_t rows, int64_t row_bytes, const void* d_src, int64_t src_pitch,
+                            const int32_t* d_idx, void* d_dst, int64_t dst_pitch) {
+  if (int rc = check_ctx(c)) return rc;
+  DeviceGuard dg(c->device);
+  return gather_rows_launch(c, rows, row_bytes, d_src, src_pitch, d_idx, d_dst, dst_pitch);
 }
 
 GSG_API int gsg_subgraph_upload_device(gsg_ctx_t c, int32_t n, int64_t nnz, const int64_t* d_indptr,

@@ -134,13 +134,19 @@ struct ProfScope {
       c->prof.flops[c->prof_row] += flops;
     }
     a = c->prof.get();
-    // external records stay timing events when the launches are captured into a CUDA graph
-    cudaEventRecordWithFlags(a, c->stream, cudaEventRecordExternal);
+    record(a);
+  }
+  // inside a stream capture, external records stay timing events of the replayed graph
+  void record(cudaEvent_t e) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &st);
+    if (st == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal);
+    else cudaEventRecord(e, c->stream);
   }
   ~ProfScope() {
     if (!a) return;
     cudaEvent_t b = c->prof.get();
-    cudaEventRecordWithFlags(b, c->stream, cudaEventRecordExternal);
+    record(b);
     c->prof.recs.push_back({cls, c->prof_row, c->prof_row >= 0 ? 2 : 1, a, b});
   }
 };
@@ -162,6 +168,8 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
                 const void* B, int64_t ldb, int transB, float* C, int64_t ldc, void* Clp, int64_t ldclp,
                 int precision, int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate);
 int to_bf16_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t lds, void* dst, int64_t ldd);
+int gather_rows_launch(gsg_ctx* ctx, int rows, int64_t row_bytes, const void* src, int64_t src_pitch,
+                       const int32_t* idx, void* dst, int64_t dst_pitch);
 int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh, const float* H, int64_t ldh,
                 float* dZ, int64_t lddz, void* dZlp, int64_t lddzlp);
 int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64_t lds, const void* labels,

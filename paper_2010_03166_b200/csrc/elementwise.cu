@@ -108,7 +108,42 @@ __global__ void __launch_bounds__(1024) k_head_final(int nblocks, int n, const f
   (void)n;
 }
 
+// dst row r = src row idx[r] (row_bytes each): 16-byte vectors when every address and pitch is
+// 16-byte aligned, bytes otherwise. One warp per row.
+__global__ void k_gather_rows(int rows, int64_t row_bytes, const uint8_t* __restrict__ src, int64_t sp,
+                              const int32_t* __restrict__ idx, uint8_t* __restrict__ dst, int64_t dp, int vec) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+    const uint8_t* s = src + (int64_t)__ldg(idx + r) * sp;
+    uint8_t* d = dst + (int64_t)r * dp;
+    if (vec) {
+      for (int64_t k = lane; k < row_bytes / 16; k += 32)
+        reinterpret_cast<uint4*>(d)[k] = __ldg(reinterpret_cast<const uint4*>(s) + k);
+    } else {
+      for (int64_t k = lane; k < row_bytes; k += 32) d[k] = s[k];
+    }
+  }
+}
+
 }  // namespace
+
+int gather_rows_launch(gsg_ctx* ctx, int rows, int64_t row_bytes, const void* src, int64_t src_pitch,
+                       const int32_t* idx, void* dst, int64_t dst_pitch) {
+  GSG_CHECK(rows >= 0 && row_bytes >= 0, GSG_EINVAL, "negative gather size");
+  if (rows == 0 || row_bytes == 0) return GSG_OK;
+  GSG_CHECK(src && idx && dst, GSG_EINVAL, "gather: NULL argument");
+  GSG_CHECK(src_pitch >= row_bytes && dst_pitch >= row_bytes, GSG_EINVAL, "gather: pitch < row_bytes");
+  const int vec = ((uintptr_t)src | (uintptr_t)dst | src_pitch | dst_pitch | row_bytes) % 16 == 0;
+  ProfScope ps(ctx, GSG_K_OTHER, 2.0 * rows * row_bytes + 4.0 * rows, 0.0);
+  int grid = (int)(((int64_t)rows * 32 + 255) / 256);
+  if (grid > ctx->num_sms * 16) grid = ctx->num_sms * 16;
+  k_gather_rows<<<grid, 256, 0, ctx->stream>>>(rows, row_bytes, (const uint8_t*)src, src_pitch, idx, (uint8_t*)dst,
+                                               dst_pitch, vec);
+  count_launch(ctx);
+  GSG_CUDA(cudaGetLastError());
+  return GSG_OK;
+}
 
 int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh, const float* H, int64_t ldh, float* dZ,
                 int64_t lddz, void* dZlp, int64_t lddzlp) {

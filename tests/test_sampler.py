@@ -129,3 +129,42 @@ def test_gpu_sample_trains():
     ctx.spmm(sg, torch.from_numpy(X).cuda(), Y)
     ref = orc.spmm(A, X)
     assert np.abs(Y.cpu().numpy() - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+@pytest.mark.gpu
+def test_gpu_sample_assign_and_gather():
+    """A GPU sample refills an existing subgraph from device arrays (gsg_subgraph_assign with
+    device pointers) bit for bit, and gsg_gather_rows builds X_s = X[V_s] and the labels
+    (Alg. 1 line 5) exactly like a host gather of the same rows."""
+    import torch
+    import paper_2010_03166_b200 as gsg
+    cfg = wl.CONFIGS[1]
+    p = wl.parent_for(cfg).csr()
+    ctx = gsg.Context(0)
+    pg = gsg.ParentGraph(ctx, p.indptr, p.indices)
+    batch = pg.sample(cfg.n, cfg.m, 123, count=2)
+    g0 = wl.sample_subgraph(cfg)
+    sg = ctx.upload(g0.indptr, g0.indices)
+    rng = np.random.default_rng(5)
+    Xp = rng.standard_normal((p.n, 50)).astype(np.float32)
+    Lp = rng.integers(0, 255, size=(p.n, 7), dtype=np.uint8)
+    Xpd = torch.zeros((p.n, 56), device="cuda")[:, :50]
+    Xpd.copy_(torch.from_numpy(Xp))
+    Lpd = torch.from_numpy(Lp).cuda()
+    for k in range(2):
+        info = batch.get(k)
+        ip, ix, nd = (t.cpu().numpy() for t in batch.tensors(k))
+        sg.assign(info["n"], info["nnz"], info["d_indptr"], info["d_indices"])
+        sg.normalize()
+        ref = orc.normalize(ip, ix, orc.NORM_ROW_SELF)
+        dip, dix, _, _ = sg.download()
+        assert np.array_equal(dip, ref.indptr) and np.array_equal(dix, ref.idx)
+        Xs = torch.zeros((info["n"], 56), device="cuda")[:, :50]
+        Ls = torch.zeros((info["n"], 7), dtype=torch.uint8, device="cuda")
+        ctx.gather_rows(Xpd, info["d_nodes"], Xs, info["n"])
+        ctx.gather_rows(Lpd, info["d_nodes"], Ls, info["n"])
+        assert np.array_equal(Xs.cpu().numpy(), Xp[nd])
+        assert np.array_equal(Ls.cpu().numpy(), Lp[nd])
+    with pytest.raises(gsg.GsgError):  # device arrays cannot be validated on the host
+        info = batch.get(0)
+        sg.assign(info["n"], info["nnz"], info["d_indptr"], info["d_indices"], validate=True)
