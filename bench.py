@@ -291,7 +291,8 @@ def main():
                     help="gpu: additionally time a training loop whose subgraphs are frontier-sampled on the GPU "
                          "(NEXT #3) from a device-resident parent graph, features gathered from a parent feature "
                          "matrix in HBM, a fresh subgraph every step")
-    ap.add_argument("--sampler-pool", type=int, default=64, help="subgraphs per GPU sampling call (--sampler gpu)")
+    ap.add_argument("--sampler-pool", type=int, default=296,
+                    help="subgraphs per GPU sampling call (--sampler gpu; 2 per SM keeps the latency-bound sampler busy)")
     ap.add_argument("--flush-l2", action="store_true",
                     help="flush L2 (write a 2x-L2 buffer) before every step of the per-step timing pass")
     args = ap.parse_args()
