@@ -32,6 +32,24 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL prints a version banner on stdout at communicator init unless told otherwise; the driver
+# reads exactly one JSON line from stdout.
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+
+
+class stdout_to_stderr:
+    """Route file descriptor 1 to stderr for the duration (library banners, e.g. NCCL's)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+        return False
 
 import workload as wl  # noqa: E402
 
@@ -285,6 +303,11 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
+    ap.add_argument("--no-comm-overlap", action="store_true",
+                    help="issue the gradient all-reduce on the compute stream after each step (default: on a "
+                         "communication stream, overlapping the next step's forward)")
+    ap.add_argument("--nccl-self", action="store_true",
+                    help="N = 1: build a 1-rank NCCL communicator so the all-reduce path (a9) runs and is timed")
     ap.add_argument("--batch", type=int, default=1,
                     help="B independent subgraphs per step as one block-diagonal graph (SURVEY §8(d) batched variant)")
     ap.add_argument("--sampler", default="host", choices=["host", "gpu"],
@@ -311,7 +334,8 @@ def main():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        with stdout_to_stderr():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     t_setup = time.time()
 
@@ -346,9 +370,20 @@ def main():
                          weights=inputs[0].Ws, w_mlp=inputs[0].W_mlp)
     stream.synchronize()
     comm = None
-    if world > 1:
-        uid = dp.broadcast_bytes(ctx.nccl_unique_id() if rank == 0 else None)
-        comm = ctx.nccl_comm_init(world, rank, uid)
+    if world > 1 or args.nccl_self:
+        with stdout_to_stderr():
+            uid = dp.broadcast_bytes(ctx.nccl_unique_id() if rank == 0 else None)
+            comm = ctx.nccl_comm_init(world, rank, uid)
+    # a9 overlap: the all-reduce of step i runs on a communication stream while step i+1 runs its
+    # forward; the replayed step waits for it (external event node) right before it writes the
+    # gradients again (GCNStep before_grads)
+    overlap = comm is not None and not args.no_comm_overlap and not args.no_graph
+    comm_stream = comm_ctx = ev_step = ev_ar = None
+    if overlap:
+        comm_stream = torch.cuda.Stream(device=dev)
+        comm_ctx = gsg.Context(local, comm_stream)
+        ev_step, ev_ar = torch.cuda.Event(), torch.cuda.Event()
+        ev_ar.record(comm_stream)  # creates the event (an unrecorded wait would be a no-op anyway)
 
     nnz_hat = [g.nnz + g.n for g in pool]
     nnz_raw = [g.nnz for g in pool]
@@ -359,11 +394,12 @@ def main():
                f"step working set ({act_bytes / 1e6:.0f} MB) fits the {l2_bytes / 1e6:.0f} MB L2: warm-cache numbers; "
                "step_ms_dist with --flush-l2 gives the flushed figure")
 
-    def step(i, with_comm=True):
+    def step(i, with_comm=True, wait_ar=False):
         k = i % len(pool)
         n = pool[k].n
         runner.forward_backward(sgs[k], Xd[k][:n], labels=labd[k], dH_top=None if dHd[k] is None else dHd[k][:n],
-                                comm=comm if with_comm else None)
+                                comm=comm if with_comm else None,
+                                before_grads=(lambda: ctx.wait_event(ev_ar)) if wait_ar else None)
         return runner.work_edge_features(nnz_hat[k])
 
     # ---- normalize every pool slot once (grows its device arrays outside any graph capture) ----
@@ -388,7 +424,7 @@ def main():
             for k in range(len(pool)):
                 gph = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(gph, stream=stream):
-                    step(k, with_comm=False)  # the NCCL all-reduce (a9) is issued eagerly after replay
+                    step(k, with_comm=False, wait_ar=overlap)  # a9 is issued after the replay
                 graphs.append(gph)
             graph_note = "cuda-graph replay of the step (a1-a8) + eager NCCL all-reduce (a9)"
         except Exception as e:  # noqa: BLE001
@@ -401,9 +437,19 @@ def main():
         k = i % len(pool)
         with torch.cuda.stream(stream):
             graphs[k].replay()
-        if comm is not None:
+        if overlap:
+            ev_step.record(stream)
+            comm_stream.wait_event(ev_step)
+            comm_ctx.allreduce_grads(comm, [runner.grad_flat], average=True)
+            ev_ar.record(comm_stream)
+        elif comm is not None:
             ctx.allreduce_grads(comm, [runner.grad_flat], average=True)
         return runner.work_edge_features(nnz_hat[k])
+
+    def drain_comm():
+        """The timed region ends when the last all-reduce has finished."""
+        if overlap:
+            stream.wait_event(ev_ar)
 
     for i in range(2):
         step_run(i)
@@ -420,6 +466,7 @@ def main():
         ev0.record(stream)
         for i in range(args.steps):
             work += step_run(i)
+        drain_comm()
         ev1.record(stream)
         stream.synchronize()
     launches = int(round(launches_per_step * args.steps)) if graphs is not None else ctx.launch_count() - launches0
@@ -558,6 +605,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         ework = run_e2e(args.steps, start_event=e0)
+        drain_comm()
         e1.record(stream)
         stream.synchronize()
         ems, ework_all = dp.reduce_timing(e0.elapsed_time(e1), float(ework), device=dev)
@@ -642,6 +690,9 @@ def main():
                           "nnz_hat_per_gpu": nnz_hat, "dims": cfg.dims, "head": f"{cfg.head}{cfg.classes}",
                           "parent": {"n": cfg.parent_n, "mean_deg": cfg.parent_mean_deg, "gamma": cfg.gamma},
                           "pool_per_gpu": len(pool), "parallelism": f"dp{world}",
+                          "allreduce": ("none" if comm is None else
+                                        "overlapped with the next step's forward (comm stream)" if overlap else
+                                        "after each step on the compute stream"),
                           "l2": l2_note},
                "roofline": roofline, "gemm": gemm_info, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches, "launch_mode": graph_note, "clocks": clk.summary(),

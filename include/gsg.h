@@ -111,6 +111,11 @@ GSG_API int gsg_ctx_set_stream(gsg_ctx_t ctx, void* cuda_stream);
 GSG_API void* gsg_ctx_stream(gsg_ctx_t ctx);
 /* Block until the context's stream drains; returns GSG_ECUDA for any pending fault. */
 GSG_API int gsg_ctx_sync(gsg_ctx_t ctx);
+/* Make the context stream wait for a CUDA event (cudaEvent_t) recorded on another stream. Inside
+ * a stream capture the wait becomes an external-event node of the graph (cudaEventWaitExternal),
+ * so a replayed step can wait for work issued outside the graph, e.g. the previous step's
+ * gradient all-reduce on a communication stream before the step overwrites the gradients. */
+GSG_API int gsg_ctx_wait_event(gsg_ctx_t ctx, void* cuda_event);
 /* Number of kernels this context has launched so far (evidence counter for benches). */
 GSG_API int64_t gsg_ctx_launch_count(gsg_ctx_t ctx);
 /* Kernel-class profiling (bench evidence): while enabled, every launch of the class is

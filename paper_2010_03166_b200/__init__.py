@@ -74,6 +74,7 @@ _SIGS = {
     "gsg_parent_free": (_int, [_vp]),
     "gsg_frontier_sample": (_int, [_vp, _vp, _i32, _i32, _i32, ctypes.c_uint64, _i32, ctypes.POINTER(_vp)]),
     "gsg_gather_rows": (_int, [_vp, _i32, _i64, _vp, _i64, _vp, _vp, _i64]),
+    "gsg_ctx_wait_event": (_int, [_vp, _vp]),
     "gsg_sample_get": (_int, [_vp, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_vp),
                               ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
     "gsg_sample_free": (_int, [_vp]),
@@ -396,6 +397,10 @@ class Context:
     @staticmethod
     def nccl_comm_destroy(comm: int):
         check(gsg_nccl_comm_destroy(comm))
+
+    def wait_event(self, event):
+        """Context stream waits for a torch.cuda.Event (an external-event node when capturing)."""
+        check(gsg_ctx_wait_event(self.h, event.cuda_event))
 
     def allreduce_grads(self, comm: int, tensors, average: bool = True):
         n = len(tensors)

@@ -232,6 +232,17 @@ GSG_API int gsg_ctx_sync(gsg_ctx_t c) {
   return GSG_OK;
 }
 
+GSG_API int gsg_ctx_wait_event(gsg_ctx_t c, void* ev) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(ev, GSG_EINVAL, "NULL event");
+  DeviceGuard dg(c->device);
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  GSG_CUDA(cudaStreamIsCapturing(c->stream, &st));
+  GSG_CUDA(cudaStreamWaitEvent(c->stream, static_cast<cudaEvent_t>(ev),
+                               st == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+  return GSG_OK;
+}
+
 GSG_API int64_t gsg_ctx_launch_count(gsg_ctx_t c) { return c ? c->launches : -1; }
 
 GSG_API int gsg_ctx_profile(gsg_ctx_t c, int enable) {

@@ -82,7 +82,12 @@ class GCNStep:
             self.dHLlp = padded(n_max, dims[-1], torch.bfloat16, device=dev) if bf else None
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
 
-    def forward_backward(self, sg: Subgraph, X, labels=None, dH_top=None, comm=None, normalize: bool = True):
+    def forward_backward(self, sg: Subgraph, X, labels=None, dH_top=None, comm=None, normalize: bool = True,
+                         before_grads=None):
+        """One step. `before_grads` (optional) is called right before the first write of a weight
+        gradient (the head, else the top layer's backward): bench.py uses it to make the step
+        wait for the previous step's all-reduce of the same gradient buffer, so that the
+        all-reduce overlaps this step's forward."""
         ctx, d, n = self.ctx, self.dims, sg.n
         if normalize:
             sg.normalize(GSG_NORM_ROW_SELF)
@@ -101,6 +106,8 @@ class GCNStep:
                               Plp=None if (self.Plp[l] is None or o2) else self.Plp[l][:n],
                               flags=(GSG_ORDER_A_XW if o2 else 0) | wflag)
             h = self.H[l][:n]
+        if before_grads is not None:
+            before_grads()
         if self.head != "none":
             kind = GSG_HEAD_SOFTMAX if self.head == "softmax" else GSG_HEAD_SIGMOID
             ctx.head(h, self.Wm, labels, self.S[:n], self.dS[:n], self.dWm, self.dHL[:n], n, d[-1], self.C, kind,
