@@ -15,8 +15,8 @@ def run(*args):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
                          timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
-    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
-    assert len(lines) == 1, out.stdout
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1 and lines[0].startswith("{"), out.stdout  # exactly one JSON line on stdout
     return json.loads(lines[0])
 
 
@@ -39,6 +39,13 @@ def test_ours_line():
     # counting without self loops (nnz < nnz') gives less work in the same time
     assert 0 < d["value_noself"] < d["value"]
     assert d["step_ms_dist"]["p10"] <= d["step_ms_dist"]["p50"] <= d["step_ms_dist"]["p90"]
+
+
+def test_allreduce_path_line():
+    """The a9 path (1-rank NCCL communicator, all-reduce overlapped on a comm stream) keeps stdout
+    to the one JSON line (NCCL's banner goes to stderr)."""
+    d = run("--config", "1", "--steps", "4", "--warmup", "3", "--no-cpu", "--nccl-self")
+    assert d["value"] > 0 and "overlapped" in d["config"]["allreduce"]
 
 
 def test_reference_line():
