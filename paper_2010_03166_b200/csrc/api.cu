@@ -153,6 +153,40 @@ int nccl_fail(ncclResult_t r, const char* what) {
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+// Fork / join of the context's side stream for a GEMM that only shares read-only inputs with
+// the work that follows it on the context stream: the constructor forks (the side stream waits
+// for everything enqueued so far) and redirects launches to the side stream, back() returns
+// them to the context stream, and the destructor joins -- on every exit path, so an error can
+// never leave an unjoined stream inside a graph capture.
+struct SideFork {
+  gsg_ctx* c;
+  cudaStream_t main;
+  bool on, away = false;
+  SideFork(gsg_ctx* c_, bool on_) : c(c_), main(c_->stream), on(on_) {
+    if (!on) return;
+    cudaEventRecord(c->ev_fork, main);
+    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    c->stream = c->side;
+    away = true;
+  }
+  void back() {
+    if (!away) return;
+    cudaEventRecord(c->ev_join, c->side);
+    c->stream = main;
+    away = false;
+  }
+  ~SideFork() {
+    if (!on) return;
+    back();
+    cudaStreamWaitEvent(main, c->ev_join, 0);
+  }
+};
+
+bool fork_enabled() {
+  static const bool f = !(getenv("GSG_BWD_FORK") && atoi(getenv("GSG_BWD_FORK")) == 0);
+  return f;
+}
+
 // The bf16 weight operand of a layer GEMM: the caller's own copy (GSG_W_BF16: W is bf16 with
 // ldw in bf16 elements) or a conversion into the context workspace.
 int bf16_weight(gsg_ctx* c, const float* W, int64_t ldw, int f_in, int f_out, int flags, const void** out,
@@ -584,25 +618,16 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   // dW = Pᵀ dZ (row a5) and T = dZ Wᵀ -> dX (rows a6, a7) only share read-only inputs: the dW
   // GEMM runs on the context's side stream (fork / join by events, also inside a CUDA-graph
   // capture), overlapping its fill / drain and split-K reduction with T's GEMM (config 5: -15 us
-  // per step, configs 3-4 -0.2-0.7 %, config 2 +1 %). GSG_BWD_FORK=0 serializes them (A/B).
-  static const bool fork = !(getenv("GSG_BWD_FORK") && atoi(getenv("GSG_BWD_FORK")) == 0);
-  const bool forked = fork && dX && !c->prof.on;  // profiling serializes (clean per-stage events)
-  cudaStream_t main_stream = c->stream;
-  if (forked) {
-    GSG_CUDA(cudaEventRecord(c->ev_fork, main_stream));
-    GSG_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    c->stream = c->side;
-  }
+  // per step, configs 3-4 -0.2-0.7 %, config 2 +1 %). GSG_BWD_FORK=0 serializes them (A/B);
+  // profiling serializes too (clean per-stage events).
+  SideFork fk(c, fork_enabled() && dX && !c->prof.on);
   // dW = Pᵀ dZ   (row a5): A = P stored n x f_in (MN-major), B = dZ stored n x f_out (MN-major)
   c->side_ws = true;
   rc = gemm_launch(c, f_in, f_out, n, bf16 ? Plp : (const void*)P, bf16 ? ldplp : ldp, 1, bf16 ? dZlp : (const void*)dZ,
                    bf16 ? lddzlp : lddz, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0,
                    (flags & GSG_ACCUM_DW) ? 1 : 0);
   c->side_ws = false;
-  if (forked) {
-    c->stream = main_stream;
-    GSG_CUDA(cudaEventRecord(c->ev_join, c->side));
-  }
+  fk.back();
   if (rc) return rc;
   if (!dX) return GSG_OK;
   c->prof_row = GSG_K_A6;
@@ -615,9 +640,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   if (rc) return rc;
   // dX = Âᵀ T [⊙ 1[H_below > 0]]   (row a7, fused a4 of the layer below)
   c->prof_row = GSG_K_A7;
-  rc = spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, dXlp, lddxlp, Hbelow, ldhb);
-  if (forked) GSG_CUDA(cudaStreamWaitEvent(main_stream, c->ev_join, 0));  // join
-  return rc;
+  return spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, dXlp, lddxlp, Hbelow, ldhb);  // fk joins on exit
 }
 
 GSG_API int gsg_sage_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32_t fh, const float* X, int64_t ldx,
@@ -700,25 +723,14 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
   if ((rc = head_loss_launch(c, n, C, kind, S, lds, labels, node_w, dS, loss))) return rc;
   // dW_mlp = H_Lᵀ dS and dH_L = (dS W_mlpᵀ) ⊙ 1[H_L > 0] only share read-only inputs: the first
   // runs on the side stream (fork / join, as in gsg_layer_backward; serialized while profiling)
-  static const bool fork = !(getenv("GSG_BWD_FORK") && atoi(getenv("GSG_BWD_FORK")) == 0);
-  const bool forked = fork && !c->prof.on;
-  cudaStream_t main_stream = c->stream;
-  if (forked) {
-    GSG_CUDA(cudaEventRecord(c->ev_fork, main_stream));
-    GSG_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    c->stream = c->side;
-  }
+  SideFork fk(c, fork_enabled() && !c->prof.on);
   c->side_ws = true;
   rc = gemm_launch(c, f, C, n, HL, ldh, 1, dS, lds, 0, dWm, lddw, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
   c->side_ws = false;
-  if (forked) {
-    c->stream = main_stream;
-    GSG_CUDA(cudaEventRecord(c->ev_join, c->side));
-  }
+  fk.back();
   if (rc) return rc;
-  rc = gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, GSG_PREC_TF32, GSG_EPI_MASK, HL, ldh, 0, 0);
-  if (forked) GSG_CUDA(cudaStreamWaitEvent(main_stream, c->ev_join, 0));  // join
-  return rc;
+  return gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, GSG_PREC_TF32, GSG_EPI_MASK, HL, ldh,
+                     0, 0);  // fk joins on exit
 }
 
 // ------------------------------------------------------------------------------ NCCL
