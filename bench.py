@@ -306,6 +306,8 @@ def main():
     ap.add_argument("--no-comm-overlap", action="store_true",
                     help="issue the gradient all-reduce on the compute stream after each step (default: on a "
                          "communication stream, overlapping the next step's forward)")
+    ap.add_argument("--no-relu-bits", action="store_true",
+                    help="gate the backward with the fp32 activations instead of their ReLU bitmasks (A/B)")
     ap.add_argument("--nccl-self", action="store_true",
                     help="N = 1: build a 1-rank NCCL communicator so the all-reduce path (a9) runs and is timed")
     ap.add_argument("--batch", type=int, default=1,
@@ -367,7 +369,7 @@ def main():
             if t is not None:
                 t[:inp.dH.shape[0]].copy_(torch.from_numpy(inp.dH))
         runner = GCNStep(ctx, cfg.dims, n_max, cfg.head, cfg.classes, cfg.precision, device=local,
-                         weights=inputs[0].Ws, w_mlp=inputs[0].W_mlp)
+                         weights=inputs[0].Ws, w_mlp=inputs[0].W_mlp, relu_bits=not args.no_relu_bits)
     stream.synchronize()
     comm = None
     if world > 1 or args.nccl_self:
@@ -693,6 +695,7 @@ def main():
                           "allreduce": ("none" if comm is None else
                                         "overlapped with the next step's forward (comm stream)" if overlap else
                                         "after each step on the compute stream"),
+                          "relu_gate": "fp32 activations" if args.no_relu_bits else "bitmask",
                           "l2": l2_note},
                "roofline": roofline, "gemm": gemm_info, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": launches, "launch_mode": graph_note, "clocks": clk.summary(),

@@ -93,6 +93,16 @@ enum {
   GSG_EPI_MASK = 2         /* C = (op(A) op(B)) ⊙ 1[aux > 0]         (ReLU' gate, a4)       */
 };
 
+/* ---- ReLU bitmasks -------------------------------------------------------------------- *
+ * The ReLU' gate 1[H > 0] of the backward (dZ = dH ⊙ σ'(Z), σ = ReLU) needs one bit per
+ * element of H, not H itself. A "ReLU bitmask" of an n x f matrix H is an n x ldb array of
+ * uint32 words (row-major, ldb >= ceil(f / 32)): bit i of word w of row r is 1[H[r, 32 w + i] > 0];
+ * bits of columns >= f are 0; words ldb > ceil(f/32) are never touched. Writers (the forward's
+ * ReLU epilogue, GEMM or SpMM) write every word of columns < f; readers (the backward's gates)
+ * read it in place of the fp32 matrix -- 1/32 of the bytes (config 5: 2.6 MB instead of 82 MB
+ * per gated layer). Wherever a call takes both a gate matrix and a gate bitmask, the bitmask
+ * wins and the matrix may be NULL. Results are identical bit for bit either way. */
+
 /* ---- head kinds ---------------------------------------------------------------------- */
 enum { GSG_HEAD_SOFTMAX = 0, GSG_HEAD_SIGMOID = 1 };
 
@@ -196,13 +206,15 @@ GSG_API int gsg_subgraph_free(gsg_subgraph_t sg);
  *   d_Ylp, ldylp optional bf16 copy of Y (NULL = none; ldylp % 8 == 0)
  *   d_mask, ldm  optional ReLU' gate: Y ⊙ 1[mask > 0] (NULL = none) -- used to emit the
  *                next layer's dZ directly from the transposed aggregation
+ *   d_mask_bits, ldmb  optional gate as a ReLU bitmask (ldmb words per row); overrides d_mask
  * Each output row is summed in a fixed order (bitwise reproducible run to run).
  * A subgraph with n = 0 returns GSG_OK without reading any pointer. Errors: GSG_EINVAL (not
  * normalized, f < 1, NULL / misaligned (16 B) pointers, ld < f or ld % 4 != 0, Y aliasing X),
  * GSG_EUNSUPPORTED (n * ldx * 4 >= 4 GiB: the kernel's 32-bit row byte offsets). */
 GSG_API int gsg_spmm(gsg_ctx_t ctx, gsg_subgraph_t sg, int transpose, int32_t f,
                      const float* d_X, int64_t ldx, float* d_Y, int64_t ldy,
-                     void* d_Ylp, int64_t ldylp, const float* d_mask, int64_t ldm);
+                     void* d_Ylp, int64_t ldylp, const float* d_mask, int64_t ldm,
+                     const uint32_t* d_mask_bits, int64_t ldmb);
 
 /* ==== dense contraction on tcgen05 tensor cores (rows a3 / a5 / a6) ==================== */
 /* C[M x N] = epi( op(A) op(B) ), fp32 accumulate in TMEM.
@@ -212,6 +224,8 @@ GSG_API int gsg_spmm(gsg_ctx_t ctx, gsg_subgraph_t sg, int transpose, int32_t f,
  *   precision    GSG_PREC_TF32: A, B are float*; GSG_PREC_BF16: A, B are bf16 (uint16) *
  *   d_C, ldc     fp32 output; d_Clp, ldclp optional bf16 copy (NULL = none)
  *   epilogue     GSG_EPI_*; d_aux/ldaux is the M x N gate for GSG_EPI_MASK
+ *   d_auxbits, ldauxb  GSG_EPI_MASK only: the gate as a ReLU bitmask (overrides d_aux)
+ *   d_Cbits, ldcb      GSG_EPI_RELU only: also write the ReLU bitmask of C (forces split_k = 1)
  *   split_k      0 = automatic; >= 1 forces the number of K splits (deterministic fixed-order
  *                reduction through the context workspace)
  *   accumulate   1 = C += result (before the epilogue is NOT supported with RELU/MASK)
@@ -223,6 +237,7 @@ GSG_API int gsg_gemm(gsg_ctx_t ctx, int32_t M, int32_t N, int32_t K,
                      const void* d_B, int64_t ldb, int transB,
                      float* d_C, int64_t ldc, void* d_Clp, int64_t ldclp,
                      int precision, int epilogue, const float* d_aux, int64_t ldaux,
+                     const uint32_t* d_auxbits, int64_t ldauxb, uint32_t* d_Cbits, int64_t ldcb,
                      int split_k, int accumulate);
 
 /* fp32 -> bf16 copy of a rows x cols matrix (round-to-nearest-even). */
@@ -235,17 +250,21 @@ GSG_API int gsg_to_bf16(gsg_ctx_t ctx, int32_t rows, int32_t cols, const float* 
  *   precision = GSG_PREC_BF16 additionally needs P_lp (bf16 n x f_in, ldplp) which the
  *   aggregation writes for the GEMM; H_lp (bf16 n x f_out) is optional.
  * Chain order: (ÂX)W by default; GSG_ORDER_A_XW selects Â(XW) (§7.1).
- * BF16: W is converted to bf16 per call unless GSG_W_BF16 says d_W already is bf16. */
+ * BF16: W is converted to bf16 per call unless GSG_W_BF16 says d_W already is bf16.
+ * d_Hbits, ldhbits: optional ReLU bitmask of H written by the same epilogue (NULL = none; not
+ * with GSG_NO_RELU) -- the gate the layer above's backward reads instead of H. */
 GSG_API int gsg_layer_forward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, int32_t f_out,
                               const float* d_X, int64_t ldx, const float* d_W, int64_t ldw,
                               float* d_P, int64_t ldp, void* d_Plp, int64_t ldplp,
                               float* d_H, int64_t ldh, void* d_Hlp, int64_t ldhlp,
-                              int precision, int flags);
+                              uint32_t* d_Hbits, int64_t ldhbits, int precision, int flags);
 /* Backward of one layer given the forward's P and H:
  *   dZ = dH ⊙ 1[H > 0] (skipped with GSG_DH_PREMASKED: dH is dZ),
  *   dW = Pᵀ dZ          (f_in x f_out; GSG_ACCUM_DW adds into dW),
  *   dX = Âᵀ (dZ Wᵀ)     (n x f_in; d_dX = NULL skips it, e.g. for layer 1),
- *        ⊙ 1[H_below > 0] when d_Hbelow != NULL, i.e. dX is then the layer below's dZ.
+ *        ⊙ 1[H_below > 0] when d_Hbelow != NULL, i.e. dX is then the layer below's dZ;
+ *        d_Hbelow_bits (ReLU bitmask of H_below, ldhbb words per row) gives the same gate from
+ *        1/32 of the bytes and overrides d_Hbelow.
  * BF16: d_Plp (bf16 P) is required; d_dHlp (bf16 copy of the premasked dH) is optional;
  * d_dXlp (bf16 copy of dX) is optional. T = dZ Wᵀ and masked-dZ live in the workspace. */
 GSG_API int gsg_layer_backward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, int32_t f_out,
@@ -256,6 +275,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, i
                                float* d_dW, int64_t lddw,
                                float* d_dX, int64_t lddx, void* d_dXlp, int64_t lddxlp,
                                const float* d_Hbelow, int64_t ldhb,
+                               const uint32_t* d_Hbelow_bits, int64_t ldhbb,
                                int precision, int flags);
 
 /* ==== GraphSAGE layer (Eq. 1; backward Eqs. 12-15) ====
@@ -290,13 +310,15 @@ GSG_API int gsg_sage_backward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, in
  *   d_dHlp       optional bf16 copy of dH_L (for BF16 layer backward).
  *   d_node_w     optional per-node loss weights λ_i (device float[n]; GraphSAINT loss
  *                normalization): loss = Σ_i λ_i CE_i and dS_i = λ_i (Y_i - Ybar_i) ⊙
- *                1[S_i > 0]. NULL = λ_i = 1/n (the mean above). */
+ *                1[S_i > 0]. NULL = λ_i = 1/n (the mean above).
+ *   d_HLbits     optional ReLU bitmask of H_L (ldhlb words per row): the dH_L gate is read from
+ *                it instead of H_L (identical result). */
 GSG_API int gsg_head(gsg_ctx_t ctx, int32_t n, int32_t f, int32_t C, int kind,
                      const float* d_HL, int64_t ldh, const float* d_Wmlp, int64_t ldw,
                      const void* d_labels, float* d_S, float* d_dS, int64_t lds,
                      float* d_dWmlp, int64_t lddw, float* d_dHL, int64_t lddh,
                      void* d_dHlp, int64_t lddhlp, float* d_loss, int precision,
-                     const float* d_node_w);
+                     const float* d_node_w, const uint32_t* d_HLbits, int64_t ldhlb);
 
 /* ==== GPU-side frontier sampling + induction ======================= *
  * Alg. 2 under reading R9, on the device, `count` independent samplers at once

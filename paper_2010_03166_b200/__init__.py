@@ -56,16 +56,16 @@ _SIGS = {
                                  ctypes.POINTER(_i32)]),
     "gsg_subgraph_download": (_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "gsg_subgraph_free": (_int, [_vp]),
-    "gsg_spmm": (_int, [_vp, _vp, _int, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
+    "gsg_spmm": (_int, [_vp, _vp, _int, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64]),
     "gsg_gemm": (_int, [_vp, _i32, _i32, _i32, _vp, _i64, _int, _vp, _i64, _int, _vp, _i64, _vp, _i64, _int, _int,
-                        _vp, _i64, _int, _int]),
+                        _vp, _i64, _vp, _i64, _vp, _i64, _int, _int]),
     "gsg_to_bf16": (_int, [_vp, _i32, _i32, _vp, _i64, _vp, _i64]),
     "gsg_layer_forward": (_int, [_vp, _vp, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp,
-                                 _i64, _int, _int]),
+                                 _i64, _vp, _i64, _int, _int]),
     "gsg_layer_backward": (_int, [_vp, _vp, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp,
-                                  _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _int]),
+                                  _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _int]),
     "gsg_head": (_int, [_vp, _i32, _i32, _i32, _int, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
-                        _vp, _i64, _vp, _int, _vp]),
+                        _vp, _i64, _vp, _int, _vp, _vp, _i64]),
     "gsg_sage_forward": (_int, [_vp, _vp, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int,
                                 _int]),
     "gsg_sage_backward": (_int, [_vp, _vp, _i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp,
@@ -330,19 +330,22 @@ class Context:
         check(gsg_gather_rows(self.h, rows, src.shape[1] * es, _ptr(src), src.stride(0) * es, idx_ptr, _ptr(dst),
                               dst.stride(0) * es))
 
-    def spmm(self, sg: Subgraph, X, Y, transpose: bool = False, Ylp=None, mask=None, f: int | None = None):
+    def spmm(self, sg: Subgraph, X, Y, transpose: bool = False, Ylp=None, mask=None, f: int | None = None,
+             mask_bits=None):
+        """mask_bits: ReLU bitmask (int32 tensor, n x ceil(f/32) words, see relu_bits) of the gate."""
         f = X.shape[1] if f is None else f
         check(gsg_spmm(self.h, sg.h, int(transpose), f, _ptr(X), _ld(X), _ptr(Y), _ld(Y), _ptr(Ylp) or None, _ld(Ylp),
-                       _ptr(mask) or None, _ld(mask)))
+                       _ptr(mask) or None, _ld(mask), _ptr(mask_bits) or None, _ld(mask_bits)))
 
     def gemm(self, A, B, C, transA=False, transB=False, precision=GSG_PREC_TF32, epilogue=GSG_EPI_NONE, aux=None,
-             Clp=None, split_k=0, accumulate=False, M=None, N=None, K=None):
+             Clp=None, split_k=0, accumulate=False, M=None, N=None, K=None, aux_bits=None, C_bits=None):
         M = C.shape[0] if M is None else M
         N = C.shape[1] if N is None else N
         if K is None:
             K = A.shape[0] if transA else A.shape[1]
         check(gsg_gemm(self.h, M, N, K, _ptr(A), _ld(A), int(transA), _ptr(B), _ld(B), int(transB), _ptr(C), _ld(C),
-                       _ptr(Clp) or None, _ld(Clp), precision, epilogue, _ptr(aux) or None, _ld(aux), split_k,
+                       _ptr(Clp) or None, _ld(Clp), precision, epilogue, _ptr(aux) or None, _ld(aux),
+                       _ptr(aux_bits) or None, _ld(aux_bits), _ptr(C_bits) or None, _ld(C_bits), split_k,
                        int(accumulate)))
 
     def to_bf16(self, src, dst, rows=None, cols=None):
@@ -351,17 +354,18 @@ class Context:
         check(gsg_to_bf16(self.h, rows, cols, _ptr(src), _ld(src), _ptr(dst), _ld(dst)))
 
     def layer_forward(self, sg: Subgraph, X, W, P, H, f_in: int, f_out: int, precision=GSG_PREC_TF32, Plp=None,
-                      Hlp=None, flags: int = 0):
+                      Hlp=None, flags: int = 0, H_bits=None):
         check(gsg_layer_forward(self.h, sg.h, f_in, f_out, _ptr(X), _ld(X), _ptr(W), _ld(W), _ptr(P), _ld(P),
-                                _ptr(Plp) or None, _ld(Plp), _ptr(H), _ld(H), _ptr(Hlp) or None, _ld(Hlp), precision,
-                                flags))
+                                _ptr(Plp) or None, _ld(Plp), _ptr(H), _ld(H), _ptr(Hlp) or None, _ld(Hlp),
+                                _ptr(H_bits) or None, _ld(H_bits), precision, flags))
 
     def layer_backward(self, sg: Subgraph, P, H, dH, W, dW, dX, f_in: int, f_out: int, precision=GSG_PREC_TF32,
-                       Plp=None, dHlp=None, dXlp=None, H_below=None, flags: int = 0):
+                       Plp=None, dHlp=None, dXlp=None, H_below=None, flags: int = 0, H_below_bits=None):
         check(gsg_layer_backward(self.h, sg.h, f_in, f_out, _ptr(P), _ld(P), _ptr(Plp) or None, _ld(Plp),
                                  _ptr(H) or None, _ld(H), _ptr(dH), _ld(dH), _ptr(dHlp) or None, _ld(dHlp),
                                  _ptr(W), _ld(W), _ptr(dW), _ld(dW), _ptr(dX) or None, _ld(dX), _ptr(dXlp) or None,
-                                 _ld(dXlp), _ptr(H_below) or None, _ld(H_below), precision, flags))
+                                 _ld(dXlp), _ptr(H_below) or None, _ld(H_below), _ptr(H_below_bits) or None,
+                                 _ld(H_below_bits), precision, flags))
 
     def sage_forward(self, sg: Subgraph, X, Ws, Wn, P, H, f_in: int, f_half: int, precision=GSG_PREC_TF32,
                      flags: int = 0):
@@ -376,10 +380,10 @@ class Context:
                                 precision, flags))
 
     def head(self, HL, Wm, labels, S, dS, dWm, dHL, n: int, f: int, C: int, kind: int, loss, dHlp=None,
-             precision=GSG_PREC_TF32, node_w=None):
+             precision=GSG_PREC_TF32, node_w=None, HL_bits=None):
         check(gsg_head(self.h, n, f, C, kind, _ptr(HL), _ld(HL), _ptr(Wm), _ld(Wm), _ptr(labels), _ptr(S), _ptr(dS),
                        _ld(S), _ptr(dWm), _ld(dWm), _ptr(dHL), _ld(dHL), _ptr(dHlp) or None, _ld(dHlp), _ptr(loss),
-                       precision, _ptr(node_w) or None))
+                       precision, _ptr(node_w) or None, _ptr(HL_bits) or None, _ld(HL_bits)))
 
     # ---- data parallel ----
     @staticmethod

@@ -474,20 +474,25 @@ GSG_API int gsg_subgraph_free(gsg_subgraph_t sg) {
 
 // ------------------------------------------------------------------------------ kernels
 GSG_API int gsg_spmm(gsg_ctx_t c, gsg_subgraph_t sg, int transpose, int32_t f, const float* X, int64_t ldx, float* Y,
-                     int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm) {
+                     int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, const uint32_t* mbits,
+                     int64_t ldmb) {
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   DeviceGuard dg(c->device);
-  return spmm_launch(c, sg, transpose ? 1 : 0, f, X, ldx, Y, ldy, Ylp, ldylp, mask, ldm);
+  BitsIO b;
+  b.in = mbits;
+  b.ldi = ldmb;
+  return spmm_launch(c, sg, transpose ? 1 : 0, f, X, ldx, Y, ldy, Ylp, ldylp, mask, ldm, 0, 0, b);
 }
 
 GSG_API int gsg_gemm(gsg_ctx_t c, int32_t M, int32_t N, int32_t K, const void* A, int64_t lda, int transA, const void* B,
                      int64_t ldb, int transB, float* C, int64_t ldc, void* Clp, int64_t ldclp, int precision, int epilogue,
-                     const float* aux, int64_t ldaux, int split_k, int accumulate) {
+                     const float* aux, int64_t ldaux, const uint32_t* auxbits, int64_t ldauxb, uint32_t* Cbits,
+                     int64_t ldcb, int split_k, int accumulate) {
   if (int rc = check_ctx(c)) return rc;
   DeviceGuard dg(c->device);
   return gemm_launch(c, M, N, K, A, lda, transA ? 1 : 0, B, ldb, transB ? 1 : 0, C, ldc, Clp, ldclp, precision,
-                     epilogue, aux, ldaux, split_k, accumulate);
+                     epilogue, aux, ldaux, split_k, accumulate, BitsIO{Cbits, ldcb, auxbits, ldauxb});
 }
 
 GSG_API int gsg_to_bf16(gsg_ctx_t c, int32_t rows, int32_t cols, const float* src, int64_t lds, void* dst, int64_t ldd) {
@@ -498,14 +503,19 @@ GSG_API int gsg_to_bf16(gsg_ctx_t c, int32_t rows, int32_t cols, const float* sr
 
 GSG_API int gsg_layer_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32_t f_out, const float* X, int64_t ldx,
                               const float* W, int64_t ldw, float* P, int64_t ldp, void* Plp, int64_t ldplp, float* H,
-                              int64_t ldh, void* Hlp, int64_t ldhlp, int precision, int flags) {
+                              int64_t ldh, void* Hlp, int64_t ldhlp, uint32_t* Hbits, int64_t ldhbits, int precision,
+                              int flags) {
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   GSG_CHECK(f_in >= 1 && f_out >= 1, GSG_EINVAL, "f_in=%d f_out=%d must be >= 1", f_in, f_out);
   GSG_CHECK(W && ldw >= f_out, GSG_EINVAL, "W NULL or ldw < f_out");
   GSG_CHECK(precision != GSG_PREC_BF16 || Plp || (flags & GSG_ORDER_A_XW), GSG_EINVAL,
             "BF16 forward needs the bf16 P copy (Plp)");
+  GSG_CHECK(!Hbits || !(flags & GSG_NO_RELU), GSG_EINVAL, "the H bitmask needs the ReLU (not GSG_NO_RELU)");
   DeviceGuard dg(c->device);
+  BitsIO hb;  // 1[H > 0] for the layer above's backward gate
+  hb.out = Hbits;
+  hb.ldo = ldhbits;
   const int n = sg->n;
   int rc;
   RowTag rt(c, GSG_K_A3);  // transform (a3); the aggregation calls below switch to a2
@@ -527,7 +537,7 @@ GSG_API int gsg_layer_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
     }
     if (rc) return rc;
     c->prof_row = GSG_K_A2;
-    return spmm_launch(c, sg, 0, f_out, P, ldp, H, ldh, Hlp, ldhlp, nullptr, 0, (flags & GSG_NO_RELU) ? 0 : 1);
+    return spmm_launch(c, sg, 0, f_out, P, ldp, H, ldh, Hlp, ldhlp, nullptr, 0, (flags & GSG_NO_RELU) ? 0 : 1, 0, hb);
   }
   c->prof_row = GSG_K_A2;
   rc = spmm_launch(c, sg, 0, f_in, X, ldx, P, ldp, precision == GSG_PREC_BF16 ? Plp : nullptr, ldplp, nullptr, 0);
@@ -539,16 +549,16 @@ GSG_API int gsg_layer_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
     int64_t ldwl = 0;
     if ((rc = bf16_weight(c, W, ldw, f_in, f_out, flags, &Wl, &ldwl))) return rc;
     return gemm_launch(c, n, f_out, f_in, Plp, ldplp, 0, Wl, ldwl, 0, H, ldh, Hlp, ldhlp, precision, epi,
-                       nullptr, 0, 0, 0);
+                       nullptr, 0, 0, 0, hb);
   }
-  return gemm_launch(c, n, f_out, f_in, P, ldp, 0, W, ldw, 0, H, ldh, Hlp, ldhlp, precision, epi, nullptr, 0, 0, 0);
+  return gemm_launch(c, n, f_out, f_in, P, ldp, 0, W, ldw, 0, H, ldh, Hlp, ldhlp, precision, epi, nullptr, 0, 0, 0, hb);
 }
 
 GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32_t f_out, const float* P, int64_t ldp,
                                const void* Plp, int64_t ldplp, const float* H, int64_t ldh, const float* dH, int64_t lddh,
                                const void* dHlp, int64_t lddhlp, const float* W, int64_t ldw, float* dW, int64_t lddw,
                                float* dX, int64_t lddx, void* dXlp, int64_t lddxlp, const float* Hbelow, int64_t ldhb,
-                               int precision, int flags) {
+                               const uint32_t* Hbelow_bits, int64_t ldhbb, int precision, int flags) {
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   GSG_CHECK(f_in >= 1 && f_out >= 1, GSG_EINVAL, "f_in=%d f_out=%d must be >= 1", f_in, f_out);
@@ -561,6 +571,11 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   const bool bf16 = precision == GSG_PREC_BF16;
   int rc;
   RowTag rt(c, GSG_K_A4);
+  // the layer below's ReLU' gate: its bitmask (1/32 of the bytes) when given, else H_below itself
+  BitsIO gb;
+  gb.in = Hbelow_bits;
+  gb.ldi = ldhbb;
+  const bool gate = Hbelow || Hbelow_bits;
   // dZ = dH ⊙ 1[H > 0]   (row a4)
   const float* dZ = dH;
   int64_t lddz = lddh;
@@ -608,7 +623,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
     if (rc || !dX) return rc;
     c->prof_row = GSG_K_A6;
     return gemm_launch(c, n, f_in, f_out, bf16 ? Glp : (const void*)G, ldg, 0, Wop2, ldw2, 1, dX, lddx, dXlp, lddxlp,
-                       precision, Hbelow ? GSG_EPI_MASK : GSG_EPI_NONE, Hbelow, ldhb, 0, 0);
+                       precision, gate ? GSG_EPI_MASK : GSG_EPI_NONE, Hbelow, ldhb, 0, 0, gb);
   }
   const void* Wop = W;
   int64_t ldwop = ldw;
@@ -640,7 +655,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   if (rc) return rc;
   // dX = Âᵀ T [⊙ 1[H_below > 0]]   (row a7, fused a4 of the layer below)
   c->prof_row = GSG_K_A7;
-  return spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, dXlp, lddxlp, Hbelow, ldhb);  // fk joins on exit
+  return spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, dXlp, lddxlp, Hbelow, ldhb, 0, 0, gb);  // fk joins on exit
 }
 
 GSG_API int gsg_sage_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32_t fh, const float* X, int64_t ldx,
@@ -709,7 +724,7 @@ GSG_API int gsg_sage_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
 GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, const float* HL, int64_t ldh,
                      const float* Wm, int64_t ldw, const void* labels, float* S, float* dS, int64_t lds, float* dWm,
                      int64_t lddw, float* dHL, int64_t lddh, void* dHlp, int64_t lddhlp, float* loss, int precision,
-                     const float* node_w) {
+                     const float* node_w, const uint32_t* HLbits, int64_t ldhlb) {
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(kind == GSG_HEAD_SOFTMAX || kind == GSG_HEAD_SIGMOID, GSG_EINVAL, "bad head kind %d", kind);
   GSG_CHECK(n >= 1 && f >= 1 && C >= 1, GSG_EINVAL, "bad head sizes n=%d f=%d C=%d", n, f, C);
@@ -729,8 +744,11 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
   c->side_ws = false;
   fk.back();
   if (rc) return rc;
+  BitsIO gb;  // ReLU' gate of H_L: its bitmask when given
+  gb.in = HLbits;
+  gb.ldi = ldhlb;
   return gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, GSG_PREC_TF32, GSG_EPI_MASK, HL, ldh,
-                     0, 0);  // fk joins on exit
+                     0, 0, gb);  // fk joins on exit
 }
 
 // ------------------------------------------------------------------------------ NCCL

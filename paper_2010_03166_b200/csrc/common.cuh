@@ -161,12 +161,21 @@ struct RowTag {
 
 // launch wrappers implemented in the .cu files
 int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode);
+// ReLU bitmasks (gsg.h "ReLU bitmask"): `out` receives 1[result > 0] of a ReLU epilogue, `in`
+// replaces the fp32 gate operand of a ReLU' (mask) epilogue. Strides in 32-bit words.
+struct BitsIO {
+  uint32_t* out = nullptr;
+  int64_t ldo = 0;
+  const uint32_t* in = nullptr;
+  int64_t ldi = 0;
+};
 int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, const float* X, int64_t ldx,
                 float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, int relu = 0,
-                int accum = 0);
+                int accum = 0, const BitsIO& bits = BitsIO{});
 int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA,
                 const void* B, int64_t ldb, int transB, float* C, int64_t ldc, void* Clp, int64_t ldclp,
-                int precision, int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate);
+                int precision, int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate,
+                const BitsIO& bits = BitsIO{});
 int to_bf16_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t lds, void* dst, int64_t ldd);
 int gather_rows_launch(gsg_ctx* ctx, int rows, int64_t row_bytes, const void* src, int64_t src_pitch,
                        const int32_t* idx, void* dst, int64_t dst_pitch);

@@ -132,8 +132,57 @@ struct GemmArgs {
   int mpad;         // rows per split in ws (num_m * tile rows): TMA-stored partial tiles never straddle splits
   int tma_store;    // 1: C / ws written by TMA bulk-tensor stores from swizzled smem staging
   int aux_tma;      // 1: the GSG_EPI_MASK operand is fetched by TMA (tmX) into the staging buffer
+  const uint32_t* abits;  // GSG_EPI_MASK gate as a ReLU bitmask (gsg.h "ReLU bitmask") instead of aux
+  int64_t ldab;
+  uint32_t* cbits;        // GSG_EPI_RELU: also write the bitmask 1[C > 0] (splits == 1 only)
+  int64_t ldcb;
   uint32_t idesc;
 };
+
+// 1[x_i > 0] of one 32-column epilogue chunk (col0 % 32 == 0) as a bitmask word; columns past
+// N (valid < 32) are cleared.
+// Two instructions per element: the sign bit of 0 - x (round-to-nearest: +0 for x = +-0, negative
+// iff x > 0) is funnel-shifted into the word, column 31 first.
+__device__ __forceinline__ uint32_t relu_bits(const float (&x)[32], int valid) {
+  uint32_t b = 0;
+#pragma unroll
+  for (int i = 31; i >= 0; i--) b = __funnelshift_l(__float_as_uint(__fsub_rn(0.f, x[i])), b, 1);
+  return valid >= 32 ? b : b & ((1u << valid) - 1u);
+}
+
+// wb[i] = w without dynamic register-array indexing (i < 4)
+__device__ __forceinline__ void set_word(uint32_t (&wb)[4], int i, uint32_t w) {
+  wb[0] = i == 0 ? w : wb[0];
+  wb[1] = i == 1 ? w : wb[1];
+  wb[2] = i == 2 ? w : wb[2];
+  wb[3] = i == 3 ? w : wb[3];
+}
+
+// The CPW bitmask words of one row that one epilogue warp produced for a tile (word w0 = first
+// chunk's column / 32): one 16- (8-) byte store per lane when they are all inside the row's
+// ceil(N/32) words and aligned, else one store per valid word.
+template <int CPW>
+__device__ __forceinline__ void store_words(const GemmArgs& g, int row, int w0, const uint32_t (&wb)[4]) {
+  uint32_t* p = g.cbits + (int64_t)row * g.ldcb + w0;
+  const int nw = (g.N + 31) >> 5;
+  if (w0 + CPW <= nw && ((uintptr_t)p % (4 * CPW)) == 0) {
+    if constexpr (CPW == 4) *reinterpret_cast<uint4*>(p) = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+    else if constexpr (CPW == 2) *reinterpret_cast<uint2*>(p) = make_uint2(wb[0], wb[1]);
+    else {
+#pragma unroll
+      for (int i = 0; i < CPW; i++) p[i] = wb[i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < CPW; i++) if (w0 + i < nw) p[i] = wb[i];
+  }
+}
+
+// x_i = x_i * bit i of the gate word (ReLU' from a bitmask)
+__device__ __forceinline__ void gate_bits(float (&x)[32], uint32_t m) {
+#pragma unroll
+  for (int i = 0; i < 32; i++) x[i] = (m >> i) & 1u ? x[i] : 0.f;
+}
 
 // Per-CTA configuration. CTA2 = cta_group::2: a CTA pair computes a 256 x BN tile with one
 // tcgen05.mma (M = 256); each CTA stages its 128 rows of A and half (BN/2) of B, so per-SM
@@ -361,6 +410,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const int e = warp - 4;           // epilogue warp index: staging buffers, aux barrier
     constexpr int CPW = BN / 32 / (kEpiWarps / 4);  // 32-column chunks per warp
+    static_assert(CPW >= 1 && CPW <= 4, "bitmask words per warp are kept in uint32_t[4]");
     const int c_begin = (e >> 2) * CPW;
     const uint32_t tempty_leader = CTA2 ? map_to_rank(smem_u32(&tempty[0]), 0) : 0u;
     int sbuf = 0;
@@ -376,6 +426,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row_base = mb * C::BMT + (int)rank * BM + q * 32;
       const int row = row_base + lane;
       const bool row_ok = row < g.M;
+      uint32_t wb[4] = {0u, 0u, 0u, 0u};  // ReLU bitmask words of this lane's row, one per chunk (cbits)
       for (int c = c_begin; c < c_begin + CPW; c++) {
         uint32_t v[32];
         __syncwarp();
@@ -400,6 +451,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (g.epi == GSG_EPI_RELU) {
 #pragma unroll
               for (int i = 0; i < 32; i++) x[i] = fmaxf(x[i], 0.f);
+              if (g.cbits) set_word(wb, c - c_begin, relu_bits(x, g.N - col0));
             } else if (aux_tma) {
               mbar_wait(&auxbar[e], aux_phase);
               aux_phase ^= 1;
@@ -411,6 +463,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 x[4 * j + 2] = m.z > 0.f ? x[4 * j + 2] : 0.f;
                 x[4 * j + 3] = m.w > 0.f ? x[4 * j + 3] : 0.f;
               }
+            } else if (g.epi == GSG_EPI_MASK && row_ok && g.abits) {
+              gate_bits(x, __ldg(g.abits + (int64_t)row * g.ldab + (col0 >> 5)));
             } else if (g.epi == GSG_EPI_MASK && row_ok) {
               const float* ax = g.aux + (int64_t)row * g.ldaux + col0;
               if (col0 + 32 <= g.N) {
@@ -500,6 +554,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (g.epi == GSG_EPI_RELU) {
 #pragma unroll
           for (int i = 0; i < 32; i++) x[i] = fmaxf(x[i], 0.f);
+          if (g.cbits) set_word(wb, c - c_begin, relu_bits(x, g.N - col0));
+        } else if (g.epi == GSG_EPI_MASK && g.abits) {
+          gate_bits(x, __ldg(g.abits + (int64_t)row * g.ldab + (col0 >> 5)));
         } else if (g.epi == GSG_EPI_MASK) {
           const float* ax = g.aux + (int64_t)row * g.ldaux + col0;
           if (full_chunk) {
@@ -545,6 +602,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       }
+      if (g.cbits && row_ok) store_words<CPW>(g, row, nb * (BN / 32) + c_begin, wb);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -576,6 +634,7 @@ __device__ __forceinline__ void reduce_store4(const GemmArgs& g, int row, int c,
     float y = x[j];
     if (g.accumulate) y += dst[j];
     if (g.epi == GSG_EPI_RELU) y = fmaxf(y, 0.f);
+    else if (g.epi == GSG_EPI_MASK && g.abits) y = (g.abits[(int64_t)row * g.ldab + ((c + j) >> 5)] >> ((c + j) & 31)) & 1u ? y : 0.f;
     else if (g.epi == GSG_EPI_MASK) y = g.aux[(int64_t)row * g.ldaux + c + j] > 0.f ? y : 0.f;
     dst[j] = y;
     if (g.Clp) g.Clp[(int64_t)row * g.ldclp + c + j] = __float2bfloat16_rn(y);
@@ -648,7 +707,7 @@ __global__ void k_fill_epi(GemmArgs g) {
     const int row = (int)(i / g.N), c = (int)(i % g.N);
     float y = g.accumulate ? g.C[(int64_t)row * g.ldc + c] : 0.f;
     if (g.epi == GSG_EPI_RELU) y = fmaxf(y, 0.f);
-    else if (g.epi == GSG_EPI_MASK) y = g.aux[(int64_t)row * g.ldaux + c] > 0.f ? y : 0.f;
+    else if (g.epi == GSG_EPI_MASK) y = 0.f;  // accumulate is NONE-only: y is 0 here
     g.C[(int64_t)row * g.ldc + c] = y;
     if (g.Clp) g.Clp[(int64_t)row * g.ldclp + c] = __float2bfloat16_rn(y);
   }
@@ -779,7 +838,7 @@ int dispatch_major(gsg_ctx* ctx, bool a_mn, bool b_mn, const CUtensorMap& ma, co
 
 int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
                 int transB, float* Cp, int64_t ldc, void* Clp, int64_t ldclp, int precision, int epilogue,
-                const float* aux, int64_t ldaux, int split_k, int accumulate) {
+                const float* aux, int64_t ldaux, int split_k, int accumulate, const BitsIO& bits) {
   GSG_CHECK(precision == GSG_PREC_TF32 || precision == GSG_PREC_BF16, GSG_EINVAL, "bad precision %d", precision);
   GSG_CHECK(epilogue >= GSG_EPI_NONE && epilogue <= GSG_EPI_MASK, GSG_EINVAL, "bad epilogue %d", epilogue);
   GSG_CHECK(M >= 0 && N >= 0 && K >= 0, GSG_EINVAL, "negative GEMM dims");
@@ -789,8 +848,14 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
             "C: need ldc >= N, ldc %% 4 == 0, 16B alignment (ldc=%lld N=%d)", (long long)ldc, N);
   GSG_CHECK(!Clp || (ldclp >= N && ldclp % 8 == 0 && (uintptr_t)Clp % 16 == 0), GSG_EINVAL,
             "Clp: need ldclp >= N, ldclp %% 8 == 0, 16B alignment");
-  GSG_CHECK(epilogue != GSG_EPI_MASK || (aux && ldaux >= N && ldaux % 4 == 0 && (uintptr_t)aux % 16 == 0),
-            GSG_EINVAL, "EPI_MASK needs aux with ldaux >= N, ldaux %% 4 == 0, 16B alignment");
+  const int64_t nwords = (N + 31) / 32;
+  GSG_CHECK(epilogue != GSG_EPI_MASK || bits.in ||
+                (aux && ldaux >= N && ldaux % 4 == 0 && (uintptr_t)aux % 16 == 0),
+            GSG_EINVAL, "EPI_MASK needs aux with ldaux >= N, ldaux %% 4 == 0, 16B alignment (or a bitmask gate)");
+  GSG_CHECK(!bits.in || (epilogue == GSG_EPI_MASK && bits.ldi >= nwords && (uintptr_t)bits.in % 4 == 0), GSG_EINVAL,
+            "bitmask gate needs GSG_EPI_MASK and ldauxb >= ceil(N/32) (ldauxb=%lld)", (long long)bits.ldi);
+  GSG_CHECK(!bits.out || (epilogue == GSG_EPI_RELU && bits.ldo >= nwords && (uintptr_t)bits.out % 4 == 0), GSG_EINVAL,
+            "bitmask output needs GSG_EPI_RELU and ldcb >= ceil(N/32) (ldcb=%lld)", (long long)bits.ldo);
   const bool bf16 = precision == GSG_PREC_BF16;
   ProfScope ps(ctx, GSG_K_GEMM,
                (double)(bf16 ? 2 : 4) * ((double)M * K + (double)K * N) + 4.0 * M * N, 2.0 * M * N * K);
@@ -799,8 +864,11 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   g.M = M; g.N = N; g.K = K;
   g.C = Cp; g.ldc = ldc;
   g.Clp = reinterpret_cast<__nv_bfloat16*>(Clp); g.ldclp = ldclp;
-  g.aux = aux; g.ldaux = ldaux; g.epi = epilogue; g.accumulate = accumulate;
+  g.aux = bits.in ? nullptr : aux; g.ldaux = ldaux; g.epi = epilogue; g.accumulate = accumulate;
+  g.abits = bits.in; g.ldab = bits.ldi;
+  g.cbits = bits.out; g.ldcb = bits.ldo;
   if (K == 0) {
+    if (bits.out) GSG_CUDA(cudaMemset2DAsync(bits.out, bits.ldo * 4, 0, nwords * 4, M, ctx->stream));  // ReLU(0) = 0
     k_fill_epi<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(g);
     count_launch(ctx);
     GSG_CUDA(cudaGetLastError());
@@ -847,6 +915,7 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
       if (t < best * 0.97) { best = t; splits = s; }
     }
   }
+  if (bits.out) splits = 1;  // the bitmask is written by the tile epilogue, not the split-K reduction
   if (splits > g.num_kb) splits = g.num_kb;
   g.kb_per_split = (g.num_kb + splits - 1) / splits;
   g.splits = (g.num_kb + g.kb_per_split - 1) / g.kb_per_split;  // no empty split
@@ -882,7 +951,7 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   // gate operand map (same 32 x 32 swizzled box as the store) for GSG_EPI_MASK
   CUtensorMap mx = mc;
   g.aux_tma = 0;
-  if (epilogue == GSG_EPI_MASK && g.tma_store && g.splits == 1) {
+  if (epilogue == GSG_EPI_MASK && !bits.in && g.tma_store && g.splits == 1) {
     if ((rc = make_store_map(&mx, aux, M, N, ldaux))) return rc;
     g.aux_tma = 1;
   }

@@ -56,6 +56,11 @@ struct SpmmArgs {
   float4* __restrict__ mega_ws;   // [mega row][segment][f4] partials (cap_mega rows)
   int* __restrict__ mega_ctr;     // [mega row][chunk] arrival counters (zero between launches)
   int cap_mega;                   // mega rows the workspace holds (more are processed whole)
+  const uint32_t* __restrict__ mbits;  // ReLU' gate as a bitmask (gsg.h), replaces mask
+  int64_t ldmb;
+  uint32_t* __restrict__ obits;        // relu: also OR 1[Y > 0] into this bitmask (zeroed first)
+  int64_t ldob;
+  int f;
   int w256;                  // 1: lanes gather 32-byte column pairs with 256-bit loads (X 32-B aligned, ldx % 8 == 0)
 };
 
@@ -230,8 +235,21 @@ __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int c4, fl
     acc.y = fmaxf(acc.y, 0.f);
     acc.z = fmaxf(acc.z, 0.f);
     acc.w = fmaxf(acc.w, 0.f);
+    if (a.obits) {
+      // this lane's 4 columns are one nibble of a 32-column word; 8 lanes share a word
+      uint32_t nib = (acc.x > 0.f ? 1u : 0u) | (acc.y > 0.f ? 2u : 0u) | (acc.z > 0.f ? 4u : 0u) | (acc.w > 0.f ? 8u : 0u);
+      const int valid = a.f - 4 * c4;
+      if (valid < 4) nib &= (1u << valid) - 1u;
+      if (nib) atomicOr(a.obits + (int64_t)row * a.ldob + (c4 >> 3), nib << ((c4 & 7) * 4));
+    }
   }
-  if (a.mask) {
+  if (a.mbits) {
+    const uint32_t m = __ldg(a.mbits + (int64_t)row * a.ldmb + (c4 >> 3)) >> ((c4 & 7) * 4);
+    acc.x = m & 1u ? acc.x : 0.f;
+    acc.y = m & 2u ? acc.y : 0.f;
+    acc.z = m & 4u ? acc.z : 0.f;
+    acc.w = m & 8u ? acc.w : 0.f;
+  } else if (a.mask) {
     const float4 m = __ldg(a.mask + (int64_t)row * a.ldm4 + c4);
     acc.x = m.x > 0.f ? acc.x : 0.f;
     acc.y = m.y > 0.f ? acc.y : 0.f;
@@ -457,7 +475,7 @@ int launch_k(gsg_ctx* ctx, K kern, int* occ_cache, const SpmmArgs& a, int64_t wa
 
 int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, const float* X, int64_t ldx,
                 float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, int relu,
-                int accum) {
+                int accum, const BitsIO& bits) {
   GSG_CHECK(sg->norm_mode >= 0, GSG_EINVAL, "subgraph not normalized (call gsg_subgraph_normalize)");
   GSG_CHECK(f >= 1, GSG_EINVAL, "f must be >= 1 (got %d)", f);
   if (sg->n == 0) return GSG_OK;
@@ -470,6 +488,11 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   GSG_CHECK(!mask || (ldm >= f && ldm % 4 == 0 && (uintptr_t)mask % 16 == 0), GSG_EINVAL,
             "mask needs ldm >= f, ldm %% 4 == 0 and 16-byte alignment");
   GSG_CHECK(X != Y, GSG_EINVAL, "Y must not alias X");
+  const int64_t nwords = (f + 31) / 32;
+  GSG_CHECK(!bits.in || (bits.ldi >= nwords && (uintptr_t)bits.in % 4 == 0), GSG_EINVAL,
+            "bitmask gate needs ldmb >= ceil(f/32) (ldmb=%lld)", (long long)bits.ldi);
+  GSG_CHECK(!bits.out || (relu && bits.ldo >= nwords && (uintptr_t)bits.out % 4 == 0), GSG_EINVAL,
+            "bitmask output needs the ReLU epilogue and ldob >= ceil(f/32)");
   GSG_CHECK((int64_t)sg->n * ldx * 4 < ((int64_t)1 << 32), GSG_EUNSUPPORTED,
             "X too large for 32-bit byte offsets (n * ldx * 4 >= 4 GiB)");
   // algorithmic (effective gather) bytes, SURVEY §8(d)
@@ -488,7 +511,13 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   a.ldy4 = ldy / 4;
   a.Ylp = reinterpret_cast<uint2*>(Ylp);
   a.ldylp4 = ldylp / 4;
-  a.mask = reinterpret_cast<const float4*>(mask);
+  a.mask = bits.in ? nullptr : reinterpret_cast<const float4*>(mask);
+  a.mbits = bits.in;
+  a.ldmb = bits.ldi;
+  a.obits = bits.out;
+  a.ldob = bits.ldo;
+  a.f = f;
+  if (bits.out) GSG_CUDA(cudaMemset2DAsync(bits.out, bits.ldo * 4, 0, nwords * 4, sg->n, ctx->stream));
   a.relu = relu;
   a.accum = accum;
   a.ldm4 = ldm / 4;

@@ -37,7 +37,8 @@ def padded(rows: int, f: int, dtype=torch.float32, align: int = 8, device="cuda"
 
 class GCNStep:
     def __init__(self, ctx: Context, dims: list, n_max: int, head: str = "none", classes: int = 0,
-                 precision: str = "tf32", device: int = 0, weights=None, w_mlp=None, order: str = "auto"):
+                 precision: str = "tf32", device: int = 0, weights=None, w_mlp=None, order: str = "auto",
+                 relu_bits: bool = True):
         self.ctx, self.dims, self.n_max = ctx, list(dims), n_max
         self.L = len(dims) - 1
         self.order = [chain_order(dims[l], dims[l + 1]) if order == "auto" else int(order) for l in range(self.L)]
@@ -59,6 +60,10 @@ class GCNStep:
         # backward GEMMs (GSG_W_BF16) instead of one conversion per GEMM call
         self.Wlp = [padded(dims[l], dims[l + 1], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
         self.dXlp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
+        # ReLU bitmasks of H (gsg.h): the forward epilogue writes 1[H > 0] as bits and the
+        # backward gates (SpMMᵀ of the layer above, the head's dH_L GEMM) read 1/32 of the bytes
+        self.Hb = [torch.zeros((n_max, (dims[l + 1] + 31) // 32), dtype=torch.int32, device=dev)
+                   if relu_bits and (l < self.L - 1 or head != "none") else None for l in range(self.L)]
         # all weight gradients in one flat buffer -> one allreduce (a9)
         # (rows padded to 16-byte strides; the padding is reduced along harmlessly)
         shapes = [(dims[l], dims[l + 1]) for l in range(self.L)]
@@ -104,19 +109,20 @@ class GCNStep:
             o2 = self.order[l] == 2
             ctx.layer_forward(sg, h, Wop[l], self.P[l][:n], self.H[l][:n], d[l], d[l + 1], precision=self.prec,
                               Plp=None if (self.Plp[l] is None or o2) else self.Plp[l][:n],
-                              flags=(GSG_ORDER_A_XW if o2 else 0) | wflag)
+                              flags=(GSG_ORDER_A_XW if o2 else 0) | wflag, H_bits=self._hb(l, n))
             h = self.H[l][:n]
         if before_grads is not None:
             before_grads()
         if self.head != "none":
             kind = GSG_HEAD_SOFTMAX if self.head == "softmax" else GSG_HEAD_SIGMOID
             ctx.head(h, self.Wm, labels, self.S[:n], self.dS[:n], self.dWm, self.dHL[:n], n, d[-1], self.C, kind,
-                     self.loss, dHlp=None if self.dHLlp is None else self.dHLlp[:n])
+                     self.loss, dHlp=None if self.dHLlp is None else self.dHLlp[:n], HL_bits=self._hb(self.L - 1, n))
             dH, dHlp, flags = self.dHL[:n], (None if self.dHLlp is None else self.dHLlp[:n]), GSG_DH_PREMASKED
         else:
             dH, dHlp, flags = dH_top, None, 0
         for l in range(self.L - 1, -1, -1):
-            Hb = self.H[l - 1][:n] if l > 0 else None
+            Hbits = self._hb(l - 1, n) if l > 0 else None
+            Hb = self.H[l - 1][:n] if l > 0 and Hbits is None else None
             o2 = self.order[l] == 2
             Pl = inputs[l] if o2 else self.P[l][:n]   # order 2 differentiates through X W: needs X
             Plp = None if self.Plp[l] is None else self.Plp[l][:n]
@@ -125,13 +131,16 @@ class GCNStep:
             ctx.layer_backward(sg, Pl, self.H[l][:n], dH, Wop[l], self.dW[l], self.dX[l][:n],
                                d[l], d[l + 1], precision=self.prec, Plp=Plp, dHlp=dHlp,
                                dXlp=None if self.dXlp[l] is None else self.dXlp[l][:n], H_below=Hb,
-                               flags=flags | (GSG_ORDER_A_XW if o2 else 0) | wflag)
+                               flags=flags | (GSG_ORDER_A_XW if o2 else 0) | wflag, H_below_bits=Hbits)
             dH = self.dX[l][:n]
             dHlp = None if self.dXlp[l] is None else self.dXlp[l][:n]
             flags = GSG_DH_PREMASKED  # the transposed aggregation already applied layer l-1's ReLU' gate
         if comm is not None:
             ctx.allreduce_grads(comm, [self.grad_flat], average=True)
         return self.loss
+
+    def _hb(self, l: int, n: int):
+        return None if self.Hb[l] is None else self.Hb[l][:n]
 
     def work_edge_features(self, nnz_hat: int) -> int:
         """2 * nnz' * f edge-features per layer (a2 + a7), summed over layers, where f is

@@ -211,16 +211,16 @@ def test_spmm_edge_cases(ctx):
     buf = torch.zeros(64 * g.n + 8, device="cuda")
     with pytest.raises(gsg.GsgError) as e:                                  # 16-byte alignment
         gsg.check(gsg.gsg_spmm(ctx.h, sg.h, 0, 64, buf.data_ptr() + 4, 64, empty(g.n, 64).data_ptr(), 64,
-                               None, 0, None, 0))
+                               None, 0, None, 0, None, 0))
     assert e.value.code == gsg.GSG_EINVAL
     with pytest.raises(gsg.GsgError) as e:                                  # ld < f
         gsg.check(gsg.gsg_spmm(ctx.h, sg.h, 0, 64, buf.data_ptr(), 60, empty(g.n, 64).data_ptr(), 64,
-                               None, 0, None, 0))
+                               None, 0, None, 0, None, 0))
     assert e.value.code == gsg.GSG_EINVAL
     big = ctx.upload(np.zeros((1 << 20) + 1, np.int64), np.zeros(0, np.int32)).normalize()
     with pytest.raises(gsg.GsgError) as e:                                  # 2^20 rows x 1024 x 4 B = 4 GiB
         gsg.check(gsg.gsg_spmm(ctx.h, big.h, 0, 1024, buf.data_ptr(), 1024, buf.data_ptr() + 4096, 1024,
-                               None, 0, None, 0))
+                               None, 0, None, 0, None, 0))
     assert e.value.code == gsg.GSG_EUNSUPPORTED
 
 
@@ -305,7 +305,7 @@ def test_gemm_k0(ctx):
     # M = 0 or N = 0: nothing to write, no pointer read (NULL accepted)
     for M, N in ((0, 16), (16, 0)):
         gsg.check(gsg.gsg_gemm(ctx.h, M, N, 32, None, 32, 0, None, 16, 0, None, 16, None, 0,
-                               gsg.GSG_PREC_TF32, gsg.GSG_EPI_RELU, None, 0, 0, 0))
+                               gsg.GSG_PREC_TF32, gsg.GSG_EPI_RELU, None, 0, None, 0, None, 0, 0, 0))
 
 
 # ------------------------------------------------------------------------------ layer
