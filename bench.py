@@ -396,13 +396,14 @@ def main():
                f"step working set ({act_bytes / 1e6:.0f} MB) fits the {l2_bytes / 1e6:.0f} MB L2: warm-cache numbers; "
                "step_ms_dist with --flush-l2 gives the flushed figure")
 
-    def step(i, with_comm=True, wait_ar=False):
+    def step(i, with_comm=True, wait_ar=False, input_grad=True):
         k = i % len(pool)
         n = pool[k].n
         runner.forward_backward(sgs[k], Xd[k][:n], labels=labd[k], dH_top=None if dHd[k] is None else dHd[k][:n],
                                 comm=comm if with_comm else None,
-                                before_grads=(lambda: ctx.wait_event(ev_ar)) if wait_ar else None)
-        return runner.work_edge_features(nnz_hat[k])
+                                before_grads=(lambda: ctx.wait_event(ev_ar)) if wait_ar else None,
+                                input_grad=input_grad)
+        return runner.work_edge_features(nnz_hat[k], input_grad)
 
     # ---- normalize every pool slot once (grows its device arrays outside any graph capture) ----
     with torch.cuda.stream(stream):
@@ -481,6 +482,38 @@ def main():
     _, total_noself = dp.reduce_timing(ms, float(work_noself), device=dev)
     value_noself = total_noself / (max_ms / 1e3)
     subgraphs_per_s = world * args.steps * args.batch / (max_ms / 1e3)
+
+    # ---- training mode: the same step without layer 1's input gradient dX (which
+    # training does not use), graph-replayed, all-reduce excluded; work counted without that a7 ----
+    training = None
+    if graphs is not None:
+        try:
+            tgraphs = []
+            for k in range(len(pool)):
+                gph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gph, stream=stream):
+                    step(k, with_comm=False, input_grad=False)
+                tgraphs.append(gph)
+            te0, te1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                for i in range(2):
+                    tgraphs[i % len(pool)].replay()
+                te0.record(stream)
+                for i in range(args.steps):
+                    tgraphs[i % len(pool)].replay()
+                te1.record(stream)
+            stream.synchronize()
+            tms = te0.elapsed_time(te1)
+            twork = sum(runner.work_edge_features(nnz_hat[i % len(pool)], False) for i in range(args.steps))
+            max_tms, total_twork = dp.reduce_timing(tms, float(twork), device=dev)
+            training = {"ms_per_step": max_tms / args.steps, "value": total_twork / (max_tms / 1e3),
+                        "unit": "edge_features/s",
+                        "what": "step without layer 1's input gradient dX (SURVEY R6), graph replay, "
+                                "all-reduce not included"}
+            del tgraphs
+        except Exception as e:  # noqa: BLE001
+            torch.cuda.synchronize()
+            training = {"unavailable": str(e)[:160]}
 
     # ---- per-step distribution: an event pair around every step (optionally after an L2 flush,
     # outside the bracket) -> p10 / p50 / p90 ms per step ----
@@ -703,7 +736,7 @@ def main():
                "rows_ms_per_step": {k: v["ms"] / args.steps for k, v in rows_prof.items()},
                "stage_timing": f"per-launch CUDA events ({prof_mode} pass of the same steps, dW GEMM not forked "
                                "while profiling); ms_per_step is the graph-replayed step",
-               "step_ms_dist": step_dist,
+               "step_ms_dist": step_dist, "training_mode": training,
                "value_noself": value_noself, "subgraphs_per_s": subgraphs_per_s,
                "layer_roofline_frac": layer_roof,
                "setup_s": time.time() - t_setup}

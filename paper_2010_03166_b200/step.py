@@ -59,7 +59,8 @@ class GCNStep:
         # bf16 weight copies, converted once per step and shared by each layer's forward and
         # backward GEMMs (GSG_W_BF16) instead of one conversion per GEMM call
         self.Wlp = [padded(dims[l], dims[l + 1], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
-        self.dXlp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
+        # (layer 1's dX has no consumer below it: no bf16 copy)
+        self.dXlp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf and l > 0 else None for l in range(self.L)]
         # ReLU bitmasks of H (gsg.h): the forward epilogue writes 1[H > 0] as bits and the
         # backward gates (SpMMᵀ of the layer above, the head's dH_L GEMM) read 1/32 of the bytes
         self.Hb = [torch.zeros((n_max, (dims[l + 1] + 31) // 32), dtype=torch.int32, device=dev)
@@ -88,11 +89,12 @@ class GCNStep:
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
 
     def forward_backward(self, sg: Subgraph, X, labels=None, dH_top=None, comm=None, normalize: bool = True,
-                         before_grads=None):
+                         before_grads=None, input_grad: bool = True):
         """One step. `before_grads` (optional) is called right before the first write of a weight
         gradient (the head, else the top layer's backward): bench.py uses it to make the step
         wait for the previous step's all-reduce of the same gradient buffer, so that the
-        all-reduce overlaps this step's forward."""
+        all-reduce overlaps this step's forward. `input_grad=False` skips layer 1's dX (the
+        gradient w.r.t. the input features, which training does not use)."""
         ctx, d, n = self.ctx, self.dims, sg.n
         if normalize:
             sg.normalize(GSG_NORM_ROW_SELF)
@@ -128,9 +130,10 @@ class GCNStep:
             Plp = None if self.Plp[l] is None else self.Plp[l][:n]
             if o2 and Plp is not None:
                 ctx.to_bf16(inputs[l], Plp)
-            ctx.layer_backward(sg, Pl, self.H[l][:n], dH, Wop[l], self.dW[l], self.dX[l][:n],
+            dXl = self.dX[l][:n] if (l > 0 or input_grad) else None
+            ctx.layer_backward(sg, Pl, self.H[l][:n], dH, Wop[l], self.dW[l], dXl,
                                d[l], d[l + 1], precision=self.prec, Plp=Plp, dHlp=dHlp,
-                               dXlp=None if self.dXlp[l] is None else self.dXlp[l][:n], H_below=Hb,
+                               dXlp=None if (self.dXlp[l] is None or l == 0) else self.dXlp[l][:n], H_below=Hb,
                                flags=flags | (GSG_ORDER_A_XW if o2 else 0) | wflag, H_below_bits=Hbits)
             dH = self.dX[l][:n]
             dHlp = None if self.dXlp[l] is None else self.dXlp[l][:n]
@@ -142,10 +145,15 @@ class GCNStep:
     def _hb(self, l: int, n: int):
         return None if self.Hb[l] is None else self.Hb[l][:n]
 
-    def work_edge_features(self, nnz_hat: int) -> int:
+    def work_edge_features(self, nnz_hat: int, input_grad: bool = True) -> int:
         """2 * nnz' * f edge-features per layer (a2 + a7), summed over layers, where f is
-        the width the aggregation runs at: f_in under order 1, f_out under order 2."""
-        return sum(2 * nnz_hat * (self.dims[l + 1] if self.order[l] == 2 else self.dims[l]) for l in range(self.L))
+        the width the aggregation runs at: f_in under order 1, f_out under order 2. Without the
+        input gradient, layer 1's a7 is not run under order 1 (under order 2 its G = Âᵀ dZ still
+        feeds dW)."""
+        w = sum(2 * nnz_hat * (self.dims[l + 1] if self.order[l] == 2 else self.dims[l]) for l in range(self.L))
+        if not input_grad and self.order[0] == 1:
+            w -= nnz_hat * self.dims[0]
+        return w
 
     def gemm_flops(self, n: int) -> int:
         f = 6 * sum(n * self.dims[l] * self.dims[l + 1] for l in range(self.L))

@@ -39,6 +39,8 @@ def test_ours_line():
     # counting without self loops (nnz < nnz') gives less work in the same time
     assert 0 < d["value_noself"] < d["value"]
     assert d["step_ms_dist"]["p10"] <= d["step_ms_dist"]["p50"] <= d["step_ms_dist"]["p90"]
+    t = d["training_mode"]   # the step without layer 1's dX, reported beside the full step
+    assert t["value"] > 0 and t["ms_per_step"] > 0
 
 
 def test_allreduce_path_line():

@@ -188,3 +188,21 @@ def test_graph_replay_matches_eager(cid):
     for a, b in zip(eager, replay):
         assert torch.equal(a, b)
     c.close()
+
+
+@pytest.mark.parametrize("cid", [2, 4])
+def test_training_mode_skips_input_grad(ctx, cid):
+    """input_grad=False leaves layer 1's dX unwritten and every other result (all
+    weight gradients, the loss, the other layers' dX) bit-identical."""
+    cfg, g, inp, sg, step, X, labels, dH = run_config(ctx, cid)
+    full = [t.clone() for t in step.H + step.dX[1:]] + [step.grad_flat.clone(), step.loss.clone()]
+    step.dX[0].fill_(123.0)
+    step.forward_backward(sg, X, labels=labels, dH_top=dH, input_grad=False)
+    ctx.sync()
+    part = step.H + step.dX[1:] + [step.grad_flat, step.loss]
+    for a, b in zip(full, part):
+        assert torch.equal(a, b)
+    assert bool((step.dX[0] == 123.0).all())
+    nh = g.nnz + g.n
+    assert step.work_edge_features(nh) - step.work_edge_features(nh, False) == \
+        (nh * cfg.dims[0] if step.order[0] == 1 else 0)
