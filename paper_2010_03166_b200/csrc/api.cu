@@ -124,11 +124,9 @@ struct Nccl {
   bool ok = false;
 };
 
-Nccl& nccl() {
-  static Nccl N;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+Nccl load_nccl() {
+  Nccl N;
+  {
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
@@ -144,6 +142,11 @@ Nccl& nccl() {
              N.GetErrorString;
     }
   }
+  return N;
+}
+
+Nccl& nccl() {
+  static Nccl N = load_nccl();  // resolved once, thread-safe (function-local static initialization)
   return N;
 }
 

@@ -18,6 +18,8 @@
 #include <cstdlib>
 #include <mutex>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace gsg {
@@ -794,11 +796,14 @@ int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const C
              const GemmArgs& g) {
   using C = Cfg<BN, BF16, CTA2>;
   auto kern = k_gemm<BN, BF16, A_MN, B_MN, CTA2>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // function attributes are per device: set once for each device a context uses (racing
+  // threads may both set them, which is harmless)
+  static std::atomic<uint64_t> attr_devs{0};
+  const uint64_t dbit = 1ull << (ctx->device & 63);
+  if (!(attr_devs.load(std::memory_order_acquire) & dbit)) {
     GSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     if (CTA2) GSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    attr_set = true;
+    attr_devs.fetch_or(dbit, std::memory_order_release);
   }
   const int tiles = g.num_m * g.num_n * g.splits;
   int grid;

@@ -28,6 +28,8 @@
 
 #include <cstdlib>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace gsg {
@@ -455,14 +457,14 @@ __global__ void __launch_bounds__(kThreads) k_spmm_narrow(SpmmArgs a) {
 }
 
 template <typename K>
-int launch_k(gsg_ctx* ctx, K kern, int* occ_cache, const SpmmArgs& a, int64_t warp_tasks) {
-  if (*occ_cache < 0) {
-    int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, kThreads, 0) != cudaSuccess || o < 1) o = 1;
-    *occ_cache = o;
+int launch_k(gsg_ctx* ctx, K kern, std::atomic<int>* occ_cache, const SpmmArgs& a, int64_t warp_tasks) {
+  int occ = occ_cache->load(std::memory_order_relaxed);
+  if (occ < 1) {  // resident CTAs per SM (the same on every sm_100a device this library accepts)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, 0) != cudaSuccess || occ < 1) occ = 1;
+    occ_cache->store(occ, std::memory_order_relaxed);
   }
   int64_t want = (warp_tasks + kWarps - 1) / kWarps;
-  int64_t grid = (int64_t)ctx->num_sms * *occ_cache;
+  int64_t grid = (int64_t)ctx->num_sms * occ;
   if (want < grid) grid = want;
   if (grid < 1) grid = 1;
   kern<<<(int)grid, kThreads, 0, ctx->stream>>>(a);
@@ -525,7 +527,7 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   a.n_heavy_ptr = sg->counters + kBins;
   a.bucket_counts = sg->counters;
   a.n_mega_ptr = sg->counters + kNMega;
-  static int occ_wide = -1, occ16 = -1, occ8 = -1, occ4 = -1;
+  static std::atomic<int> occ_wide{0}, occ16{0}, occ8{0}, occ4{0};
   if (a.f4 > 16) {
     a.nchunks = (a.f4 + 32 * V - 1) / (32 * V);
     {  // mega-row workspace: at most nnz' / kMegaMinDeg rows can have deg' >= kMegaMinDeg
@@ -542,8 +544,7 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
       }
     }
     a.cw = (a.f4 + a.nchunks - 1) / a.nchunks;
-    static int w256_env = -1;
-    if (w256_env < 0) { const char* ev = getenv("GSG_SPMM_W256"); w256_env = ev ? atoi(ev) : 1; }
+    static const int w256_env = getenv("GSG_SPMM_W256") ? atoi(getenv("GSG_SPMM_W256")) : 1;
     a.w256 = w256_env && (uintptr_t)X % 32 == 0 && ldx % 8 == 0;  // GSG_SPMM_W256=0: 128-bit path (A/B)
     if (a.w256) a.cw = (a.cw + 1) & ~1;  // chunks start on 32-byte column pairs
     return launch_k(ctx, k_spmm_wide, &occ_wide, a, (int64_t)sg->n * a.nchunks);
