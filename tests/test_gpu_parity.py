@@ -542,3 +542,45 @@ def test_allreduce_single_rank(ctx):
     ctx.sync()
     assert torch.equal(a, ref_a) and torch.equal(b, ref_b)
     ctx.nccl_comm_destroy(comm)
+
+
+def test_spmm_largest_offsets(ctx):
+    """Maximum size for the kernel's 32-bit row byte offsets: n * ldx * 4 just below 4 GiB
+    (n = 1,048,575 rows of 1024 fp32). Isolated rows (Â_ii = 1) must come back exactly; a
+    mega row (deg' = 2101 >= 2048: split over 8 CTAs per chunk) at the very end, whose neighbors
+    span the whole address range, and its deg-1 neighbors are checked against fp64 sums."""
+    f, n = 1024, (1 << 32) // (1024 * 4) - 1
+    hub = n - 1
+    nb = np.unique(np.linspace(0, n - 2, 2100).astype(np.int64))
+    rows = np.concatenate([np.repeat(nb, 1), np.full(nb.size, hub)])
+    cols = np.concatenate([np.full(nb.size, hub), nb])
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    ip = np.zeros(n + 1, np.int64)
+    np.add.at(ip, rows + 1, 1)
+    ip = np.cumsum(ip)
+    sg = ctx.upload(ip, cols.astype(np.int32)).normalize()
+    X = torch.empty((n, f), device="cuda").normal_(generator=torch.Generator("cuda").manual_seed(5))
+    Y = torch.empty((n, f), device="cuda")
+    probe = np.array([1, 2, n // 3 + 1, n - 3], np.int64)       # isolated rows (not in nb)
+    probe = probe[~np.isin(probe, nb)]
+    for tr in (False, True):
+        ctx.spmm(sg, X, Y, transpose=tr)
+        torch.cuda.synchronize()
+        pi = torch.from_numpy(probe).cuda()
+        assert torch.equal(Y[pi], X[pi])
+        nbt = torch.from_numpy(nb).cuda()
+        Xn = X[nbt].double().cpu().numpy()
+        Xh = X[hub].double().cpu().numpy()
+        # row-self normalization: hub row 1/(deg+1) for itself and every neighbor (a2); the
+        # transposed values (a7) take each entry's column degree: 1/2 for every neighbor
+        ref_hub = (Xh + Xn.sum(0)) / (nb.size + 1) if not tr else Xh / (nb.size + 1) + Xn.sum(0) / 2
+        got = Y[hub].double().cpu().numpy()
+        assert np.abs(got - ref_hub).max() <= 1e-5 * np.abs(ref_hub).max()
+        k = nb[-5:]
+        ref_nb = (X[torch.from_numpy(k).cuda()].double().cpu().numpy() + Xh) / 2 if not tr else \
+            X[torch.from_numpy(k).cuda()].double().cpu().numpy() / 2 + Xh / (nb.size + 1)
+        got = Y[torch.from_numpy(k).cuda()].double().cpu().numpy()
+        assert np.abs(got - ref_nb).max() <= 1e-5 * np.abs(ref_nb).max()
+    del X, Y
+    torch.cuda.empty_cache()
