@@ -584,3 +584,25 @@ def test_spmm_largest_offsets(ctx):
         assert np.abs(got - ref_nb).max() <= 1e-5 * np.abs(ref_nb).max()
     del X, Y
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("ta", [False, True])
+def test_gemm_many_rows(ctx, ta):
+    """A GEMM over a million-row operand (M = 1,048,575 x N = 96 x K = 40 and its transposed
+    reduction form K = 1,048,575): 64-bit row offsets in every epilogue / split-K path; sampled
+    rows / the full small output against fp64."""
+    g = torch.Generator("cuda").manual_seed(9)
+    big, small = (1 << 20) - 1, 40
+    A = torch.empty((big, small), device="cuda").normal_(generator=g)
+    B = torch.empty((big if ta else small, 96), device="cuda").normal_(generator=g)
+    if not ta:
+        C = torch.empty((big, 96), device="cuda")
+        ctx.gemm(A, B, C, epilogue=gsg.GSG_EPI_RELU)
+        idx = torch.tensor([0, 1, big // 2, big - 2, big - 1], device="cuda")
+        ref = np.maximum(A[idx].double().cpu().numpy() @ B.double().cpu().numpy(), 0)
+        assert rel_err(host(C[idx]), ref) <= GEMM_TOL
+    else:
+        C = torch.empty((small, 96), device="cuda")
+        ctx.gemm(A, B, C, transA=True)                             # C = Aᵀ B, K = big (split-K)
+        ref = A.double().T @ B.double()
+        assert rel_err(host(C), ref.cpu().numpy()) <= GEMM_TOL
