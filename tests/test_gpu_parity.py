@@ -606,3 +606,24 @@ def test_gemm_many_rows(ctx, ta):
         ctx.gemm(A, B, C, transA=True)                             # C = Aᵀ B, K = big (split-K)
         ref = A.double().T @ B.double()
         assert rel_err(host(C), ref.cpu().numpy()) <= GEMM_TOL
+
+
+@pytest.mark.parametrize("f,ld,off", [(68, 68, 0), (300, 300, 0), (1100, 1100, 0), (1024, 1024, 4), (200, 204, 0)])
+def test_spmm_128bit_gather_path(ctx, f, ld, off):
+    """Operands the 256-bit gather path does not take (row stride not a multiple of 8 floats, or
+    X only 16-byte aligned: `off` floats into the allocation) run the 128-bit wide path --
+    light, heavy and mega rows (a 2500-degree hub), forward and transposed, with a mask."""
+    g = star_plus_random(3000, 2500, 17)
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW_SELF)
+    sg = ctx.upload(g.indptr, g.indices).normalize(gsg.GSG_NORM_ROW_SELF)
+    rng = np.random.default_rng(f + ld + off)
+    X = rng.standard_normal((g.n, f)).astype(np.float32)
+    Hb = rng.standard_normal((g.n, f)).astype(np.float32)
+    buf = torch.full((g.n * ld + off,), float("nan"), device="cuda")
+    Xd = buf[off:].view(g.n, ld)[:, :f]
+    Xd.copy_(torch.from_numpy(X))
+    Y = torch.full((g.n, ld), float("nan"), device="cuda")[:, :f]
+    ctx.spmm(sg, Xd, Y)
+    assert rel_err(host(Y), orc.spmm(A, X)) <= SPMM_TOL
+    ctx.spmm(sg, Xd, Y, transpose=True, mask=dev(Hb))
+    assert rel_err(host(Y), np.where(Hb > 0, orc.spmm_t(A, X), 0.0)) <= SPMM_TOL
