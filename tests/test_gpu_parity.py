@@ -627,3 +627,27 @@ def test_spmm_128bit_gather_path(ctx, f, ld, off):
     assert rel_err(host(Y), orc.spmm(A, X)) <= SPMM_TOL
     ctx.spmm(sg, Xd, Y, transpose=True, mask=dev(Hb))
     assert rel_err(host(Y), np.where(Hb > 0, orc.spmm_t(A, X), 0.0)) <= SPMM_TOL
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True)])
+def test_gemm_strides_multiple_of_4(ctx, ta, tb):
+    """TF32 operands and C with row strides that are multiples of 4 floats but not of 8 (TMA's
+    16-byte rule is the only requirement), all three epilogues."""
+    rng = np.random.default_rng(31)
+    M, N, K = 700, 300, 420
+    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    aux = rng.standard_normal((M, N)).astype(np.float32)
+
+    def dev4(a):
+        r, c = a.shape
+        ld = (c + 3) // 4 * 4 + (4 if ((c + 3) // 4 * 4) % 8 == 0 else 0)   # ld % 8 == 4
+        return dev(a, ld)
+    ref = orc.gemm(A, B, transA=ta, transB=tb)
+    for epi, want in ((gsg.GSG_EPI_NONE, ref), (gsg.GSG_EPI_RELU, np.maximum(ref, 0)),
+                      (gsg.GSG_EPI_MASK, np.where(aux > 0, ref, 0))):
+        C = dev4(np.zeros((M, N), np.float32))
+        assert C.stride(0) % 8 == 4
+        ctx.gemm(dev4(A), dev4(B), C, transA=ta, transB=tb, epilogue=epi,
+                 aux=dev4(aux) if epi == gsg.GSG_EPI_MASK else None, K=K)
+        assert rel_err(host(C), want) <= GEMM_TOL
