@@ -227,7 +227,9 @@ __device__ __forceinline__ float4 group_row_sum(const SpmmArgs& a, int b, int e,
   return acc;
 }
 
-__device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int c4, float4 acc) {
+// mw: the gate word of (row, c4) already loaded by the caller (bitmask gate), else nullptr
+__device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int c4, float4 acc,
+                                          const uint32_t* mw = nullptr) {
   if (a.accum) {
     const float4 o = a.Y[(int64_t)row * a.ldy4 + c4];
     acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
@@ -246,7 +248,7 @@ __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int c4, fl
     }
   }
   if (a.mbits) {
-    const uint32_t m = __ldg(a.mbits + (int64_t)row * a.ldmb + (c4 >> 3)) >> ((c4 & 7) * 4);
+    const uint32_t m = (mw ? *mw : __ldg(a.mbits + (int64_t)row * a.ldmb + (c4 >> 3))) >> ((c4 & 7) * 4);
     acc.x = m & 1u ? acc.x : 0.f;
     acc.y = m & 2u ? acc.y : 0.f;
     acc.z = m & 4u ? acc.z : 0.f;
@@ -386,6 +388,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
     const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
     const int b = a.rowptr[row], e = a.rowptr[row + 1];
     int c4, c4b;
+    // the gate word is loaded before the gathers (its latency hides behind them) instead of
+    // after them, where it would add a dependent round trip to every task
+    uint32_t mw0 = 0, mw1 = 0;
+    if (a.mbits) {
+      const uint32_t* mr = a.mbits + (int64_t)row * a.ldmb;
+      const int g0 = a.w256 ? c0 + 2 * lane : c0 + lane;
+      if (g0 < lim) mw0 = __ldg(mr + (g0 >> 3));
+      if (!a.w256 && g0 + 32 < lim) mw1 = __ldg(mr + ((g0 + 32) >> 3));
+    }
     Acc A;
     if (a.w256) {
       c4 = c0 + 2 * lane;
@@ -399,8 +410,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
       else
         warp_row_sum<false>(a, st, b, e, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
     }
-    if (c4 < lim) store_row(a, row, c4, acc_part(A, 0));
-    if (c4b < lim) store_row(a, row, c4b, acc_part(A, 1));
+    if (c4 < lim) store_row(a, row, c4, acc_part(A, 0), &mw0);
+    if (c4b < lim) store_row(a, row, c4b, acc_part(A, 1), a.w256 ? &mw0 : &mw1);
   }
 }
 
