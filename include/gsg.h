@@ -209,8 +209,9 @@ GSG_API int gsg_subgraph_free(gsg_subgraph_t sg);
  *   d_mask_bits, ldmb  optional gate as a ReLU bitmask (ldmb words per row); overrides d_mask
  * Each output row is summed in a fixed order (bitwise reproducible run to run).
  * A subgraph with n = 0 returns GSG_OK without reading any pointer. Errors: GSG_EINVAL (not
- * normalized, f < 1, NULL / misaligned (16 B) pointers, ld < f or ld % 4 != 0, Y aliasing X),
- * GSG_EUNSUPPORTED (n * ldx * 4 >= 4 GiB: the kernel's 32-bit row byte offsets). */
+ * normalized, f < 1, NULL / misaligned (16 B) pointers, ld < f or ld % 4 != 0, Y aliasing X,
+ * ldmb < ceil(f/32) or a bitmask not 4-byte aligned), GSG_EUNSUPPORTED (n * ldx * 4 >= 4 GiB:
+ * the kernel's 32-bit row byte offsets). */
 GSG_API int gsg_spmm(gsg_ctx_t ctx, gsg_subgraph_t sg, int transpose, int32_t f,
                      const float* d_X, int64_t ldx, float* d_Y, int64_t ldy,
                      void* d_Ylp, int64_t ldylp, const float* d_mask, int64_t ldm,
@@ -231,7 +232,8 @@ GSG_API int gsg_spmm(gsg_ctx_t ctx, gsg_subgraph_t sg, int transpose, int32_t f,
  *   accumulate   1 = C += result (before the epilogue is NOT supported with RELU/MASK)
  * K = 0 writes epi(0); M = 0 or N = 0 returns GSG_OK without reading any pointer. Errors:
  * GSG_EINVAL (bad precision / epilogue, negative dims, ld or 16-byte alignment violations,
- * accumulate with an epilogue), GSG_ECUDA (launch failure). */
+ * accumulate with an epilogue, d_auxbits without GSG_EPI_MASK or d_Cbits without GSG_EPI_RELU,
+ * bitmask strides below ceil(N/32) words), GSG_ECUDA (launch failure). */
 GSG_API int gsg_gemm(gsg_ctx_t ctx, int32_t M, int32_t N, int32_t K,
                      const void* d_A, int64_t lda, int transA,
                      const void* d_B, int64_t ldb, int transB,
