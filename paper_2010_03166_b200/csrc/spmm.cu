@@ -276,7 +276,12 @@ __device__ __forceinline__ float4 acc_part(const Acc& A, int q) {
 }
 
 // Full-warp kernel (f > 64): chunk = up to 64 float4 (256 columns), lane owns c4 and c4 + 32.
-__global__ void __launch_bounds__(kThreads, 2) k_spmm_wide(SpmmArgs a) {
+// MINB resident 8-warp CTAs per SM: 3 (80 registers per thread, a few spill bytes) keeps more
+// gathers in flight on large problems (config 5 2.973 -> 2.945 ms, config 3 0.619 -> 0.594 ms);
+// 2 (128 registers) wins when a warp gets fewer than ~6 light tasks (config 2 SpMM 35 vs 39 µs,
+// config 1). profiles/r01_spmm_occupancy_ab.txt.
+template <int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
   __shared__ __align__(16) int2 stage[kWarps][32];
   __shared__ float4 part[kWarps][32 * V];
   const int lane = threadIdx.x & 31;
@@ -538,7 +543,7 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   a.n_heavy_ptr = sg->counters + kBins;
   a.bucket_counts = sg->counters;
   a.n_mega_ptr = sg->counters + kNMega;
-  static std::atomic<int> occ_wide{0}, occ16{0}, occ8{0}, occ4{0};
+  static std::atomic<int> occ_wide{0}, occ_wide3{0}, occ16{0}, occ8{0}, occ4{0};
   if (a.f4 > 16) {
     a.nchunks = (a.f4 + 32 * V - 1) / (32 * V);
     {  // mega-row workspace: at most nnz' / kMegaMinDeg rows can have deg' >= kMegaMinDeg
@@ -558,7 +563,9 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
     static const int w256_env = getenv("GSG_SPMM_W256") ? atoi(getenv("GSG_SPMM_W256")) : 1;
     a.w256 = w256_env && (uintptr_t)X % 32 == 0 && ldx % 8 == 0;  // GSG_SPMM_W256=0: 128-bit path (A/B)
     if (a.w256) a.cw = (a.cw + 1) & ~1;  // chunks start on 32-byte column pairs
-    return launch_k(ctx, k_spmm_wide, &occ_wide, a, (int64_t)sg->n * a.nchunks);
+    const int64_t tasks = (int64_t)sg->n * a.nchunks;
+    if (tasks >= 6LL * ctx->num_sms * 3 * kWarps) return launch_k(ctx, k_spmm_wide<3>, &occ_wide3, a, tasks);
+    return launch_k(ctx, k_spmm_wide<2>, &occ_wide, a, tasks);
   }
   a.nchunks = 1;
   a.cw = a.f4;
