@@ -87,6 +87,32 @@ def test_row_modes_match_dense_definition():
     np.testing.assert_allclose(R.dense().sum(1)[nz], 1.0, atol=1e-15)
 
 
+def test_values_mode_is_the_given_matrix():
+    """GSG_NORM_VALUES (weighted Â): Â_ij = value of the stored edge (i, j) and no
+    self loop. Pinned against a dense matrix built here directly from (indptr, indices, values)
+    by numpy fancy indexing -- not through AHat.dense() -- and through the products: ÂX and ÂᵀT
+    with numpy's matmul of that matrix (values deliberately asymmetric: v(i,j) != v(j,i))."""
+    g = rand_graph(70, 6.0, 21)
+    rng = np.random.default_rng(22)
+    vals = rng.uniform(-1.0, 2.0, g.nnz)
+    rows = np.repeat(np.arange(g.n), np.diff(g.indptr))
+    D = np.zeros((g.n, g.n))
+    D[rows, g.indices] = vals
+    assert not np.allclose(D, D.T)
+    A = orc.normalize(g.indptr, g.indices, orc.NORM_VALUES, vals)
+    np.testing.assert_array_equal(A.indptr, g.indptr)
+    np.testing.assert_array_equal(A.idx, g.indices)
+    np.testing.assert_array_equal(A.val, vals)
+    np.testing.assert_array_equal(A.dense(), D)
+    X = rng.standard_normal((g.n, 5))
+    np.testing.assert_allclose(orc.spmm(A, X), D @ X, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(orc.spmm_t(A, X), D.T @ X, rtol=0, atol=1e-12)
+    vt = orc.transpose_alg4(A)
+    DT = np.zeros((g.n, g.n))
+    DT[rows, g.indices] = vt
+    np.testing.assert_array_equal(DT, D.T)
+
+
 # ------------------------------------------------------------------------------ Alg. 4
 def test_alg4_two_node_swap():
     # SPEC S:77: data for (0,1)=x, (1,0)=y -> transposed data has y at (0,1)'s slot

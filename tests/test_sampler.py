@@ -6,6 +6,8 @@ brute-force induction, agreement with the independent workload generator's induc
 gpu: the device sampler (gsg_frontier_sample) reproduces the oracle bit for bit -- same
 counter-based draws (include/gsg.h) -- and its output trains through the C ABI.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -86,6 +88,149 @@ def test_oracle_induce_bruteforce_and_independent_impl():
     assert got == expect
     w = wl.Parent.from_csr(p).induce(v.astype(np.int64))  # the generator's own (host C++) induction
     assert np.array_equal(w.indptr, ip) and np.array_equal(w.indices, ix)
+
+
+# ---------------------------------------------------------------- Alg. 2 line 4 pin
+# Brute force on a tiny parent: the exact distribution of the sampled node set V_s, computed by
+# propagating probability mass through Alg. 2's Markov chain (R9 reading) with the frontier pop
+# written as P:377 states it -- u in FS with probability deg(u) / sum_{v in FS} deg(v) -- and
+# compared with the oracle's empirical distribution over many seeds (chi-square). A uniform pop
+# (or a pop by any other weight) gives a different distribution on this graph; the mutation test
+# below builds exactly that mutant from oracle.c and checks that the same test rejects it.
+_TINY_EDGES = [(0, 1), (0, 2), (0, 3), (0, 4), (0, 5), (1, 6), (6, 7), (7, 8)]
+
+
+def _tiny_parent():
+    n = 9
+    adj = [[] for _ in range(n)]
+    for a, b in _TINY_EDGES:
+        adj[a].append(b)
+        adj[b].append(a)
+    indptr = np.zeros(n + 1, np.int64)
+    indptr[1:] = np.cumsum([len(a) for a in adj])
+    indices = np.array([v for a in adj for v in sorted(a)], np.int32)
+    return indptr, indices, [sorted(a) for a in adj]
+
+
+def _exact_vs_distribution(adj, n_budget, m, pop_weight):
+    """P(V_s = S) for Alg. 2 (R9): FS_0 = m distinct non-isolated nodes, ordered, uniform; then
+    repeat {pop slot s w.p. pop_weight(FS[s]) / sum; u' uniform neighbor of FS[s]; FS[s] <- u';
+    V_s <- V_s ∪ {u'}} until |V_s| = n_budget. Mass propagation over (FS, V_s) states."""
+    import itertools
+    noniso = [v for v in range(len(adj)) if adj[v]]
+    start = list(itertools.permutations(noniso, m))
+    cur = {}
+    for fs in start:
+        key = (fs, frozenset(fs))
+        cur[key] = cur.get(key, 0.0) + 1.0 / len(start)
+    done = {}
+    for _ in range(5000):
+        nxt = {}
+        for (fs, vs), p in cur.items():
+            w = [pop_weight(u) for u in fs]
+            tot = float(sum(w))
+            for s, u in enumerate(fs):
+                for up in adj[u]:
+                    q = p * (w[s] / tot) / len(adj[u])
+                    nfs = fs[:s] + (up,) + fs[s + 1:]
+                    nvs = vs | {up}
+                    if len(nvs) == n_budget:
+                        k = tuple(sorted(nvs))
+                        done[k] = done.get(k, 0.0) + q
+                    else:
+                        nxt[(nfs, nvs)] = nxt.get((nfs, nvs), 0.0) + q
+        cur = nxt
+        if sum(cur.values()) < 1e-13:
+            break
+    assert sum(cur.values()) < 1e-9
+    return done
+
+
+def _chi2_pvalue(samples, dist, n_draws):
+    from scipy.stats import chi2
+    keys = sorted(dist, key=lambda k: -dist[k])
+    obs, exp = [], []
+    rest_o, rest_e = 0.0, 0.0
+    for k in keys:
+        e = dist[k] * n_draws
+        if e >= 10:
+            obs.append(samples.get(k, 0))
+            exp.append(e)
+        else:
+            rest_o += samples.get(k, 0)
+            rest_e += e
+    unknown = sum(c for k, c in samples.items() if k not in dist)
+    obs.append(rest_o + unknown)
+    exp.append(rest_e)
+    obs, exp = np.array(obs, float), np.array(exp, float)
+    if exp[-1] < 1e-12:
+        assert obs[-1] == 0, "the sampler produced a node set the brute force gives probability 0"
+        obs, exp = obs[:-1], exp[:-1]
+    stat = float(((obs - exp) ** 2 / exp).sum())
+    return float(chi2.sf(stat, len(obs) - 1))
+
+
+def _oracle_histogram(sample_fn, indptr, indices, n_budget, m, draws):
+    h = {}
+    for s in range(draws):
+        v = sample_fn(indptr, indices, n_budget, m, 1, 1000 + s)
+        k = tuple(int(x) for x in v)
+        h[k] = h.get(k, 0) + 1
+    return h
+
+
+_N_BUDGET, _M, _DRAWS = 5, 2, 30000
+
+
+def test_oracle_frontier_pop_degree_proportional_bruteforce():
+    """Alg. 2 line 4: the oracle's V_s distribution equals the exact Markov-chain
+    distribution with degree-proportional pops (chi-square, 30K seeds), and is far from the
+    uniform-pop distribution on the same graph."""
+    indptr, indices, adj = _tiny_parent()
+    deg = [len(a) for a in adj]
+    exact = _exact_vs_distribution(adj, _N_BUDGET, _M, lambda u: deg[u])
+    uniform = _exact_vs_distribution(adj, _N_BUDGET, _M, lambda u: 1)
+    assert abs(sum(exact.values()) - 1.0) < 1e-9
+    # the two readings are well separated at this sample size (expected chi-square >> threshold)
+    sep = _DRAWS * sum((uniform.get(k, 0.0) - p) ** 2 / p for k, p in exact.items())
+    assert sep > 500, sep
+    h = _oracle_histogram(orc.frontier_sample, indptr, indices, _N_BUDGET, _M, _DRAWS)
+    assert _chi2_pvalue(h, exact, _DRAWS) > 1e-4
+    assert _chi2_pvalue(h, uniform, _DRAWS) < 1e-12
+
+
+def test_oracle_frontier_pop_uniform_mutant_is_rejected(tmp_path):
+    """Mutation test: oracle.c rebuilt with the pop weight deg(u) replaced by 1 (a uniform pop)
+    fails the brute-force pin above -- the pin demonstrably detects the mutant."""
+    import ctypes
+    import subprocess
+    src = open(os.path.join(os.path.dirname(orc.__file__), "oracle.c")).read()
+    pop_total = "total += indptr[fs[i] + 1] - indptr[fs[i]];"
+    pop_cum = "cum += indptr[fs[slot] + 1] - indptr[fs[slot]];"
+    assert src.count(pop_total) == 1 and src.count(pop_cum) == 1, "pop code moved: update the mutation"
+    mut = src.replace(pop_total, "total += 1;").replace(pop_cum, "cum += 1;")
+    (tmp_path / "m.c").write_text(mut)
+    so = tmp_path / "libm.so"
+    subprocess.run(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-o", str(so), str(tmp_path / "m.c"),
+                    "-lm"], check=True)
+    L = ctypes.CDLL(str(so))
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    L.oracle_frontier_sample.restype = i32
+    L.oracle_frontier_sample.argtypes = [i64, vp, vp, i32, i32, i32, ctypes.c_uint64, vp]
+
+    def mutant(ip, ix, n, m, clip, seed):
+        out = np.empty(n, np.int32)
+        nv = L.oracle_frontier_sample(ip.shape[0] - 1, ip.ctypes.data_as(vp), ix.ctypes.data_as(vp), n, m, clip,
+                                      seed, out.ctypes.data_as(vp))
+        return out[:nv]
+
+    indptr, indices, adj = _tiny_parent()
+    deg = [len(a) for a in adj]
+    exact = _exact_vs_distribution(adj, _N_BUDGET, _M, lambda u: deg[u])
+    uniform = _exact_vs_distribution(adj, _N_BUDGET, _M, lambda u: 1)
+    h = _oracle_histogram(mutant, indptr, indices, _N_BUDGET, _M, _DRAWS)
+    assert _chi2_pvalue(h, exact, _DRAWS) < 1e-12      # the degree-proportional pin rejects it
+    assert _chi2_pvalue(h, uniform, _DRAWS) > 1e-4     # and it is what it claims to be
 
 
 # ------------------------------------------------------------------------------ GPU
