@@ -541,6 +541,8 @@ def main():
     # captured in one CUDA graph with the event records as graph nodes and replayed once, so the
     # per-stage times carry no host launch gaps (eager fallback if capture fails) ----
     pv0, pv1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    drain_comm()  # the last overlapped all-reduce must finish before grad_flat is rewritten
+    stream.synchronize()
     ctx.profile(True)
     prof_mode = "eager"
     if graphs is not None:

@@ -333,7 +333,8 @@ GSG_API int gsg_head(gsg_ctx_t ctx, int32_t n, int32_t f, int32_t C, int kind,
  *   clip |V_s| to a multiple of `clip` by uniformly random removals (§7.2);
  *   induce G_s on V_s with ascending local ids (Alg. 2 line 9).
  * Random draws come from a counter-based generator: draw j of iteration i of sampler k is
- *   r = mix64(seed_k XOR mix64(4 i + j)),  seed_k = seed + k,
+ *   r = mix64(seed_k XOR mix64(4 i + j)),  seed_k = mix64(mix64(seed) + k)
+ *   (so calls with nearby seeds draw unrelated subgraphs),
  *   mix64 = splitmix64 finalizer (z += 0x9E3779B97F4A7C15; z ^= z>>30; z *= 0xBF58476D1CE4E5B9;
  *           z ^= z>>27; z *= 0x94D049BB133111EB; z ^= z>>31),
  *   uniform integer below N (N < 2^32): ((r >> 32) * N) >> 32;
@@ -346,7 +347,7 @@ typedef struct gsg_sample* gsg_sample_t;
 GSG_API int gsg_parent_upload(gsg_ctx_t ctx, int64_t N, int64_t nnz, const int64_t* h_indptr,
                               const int32_t* h_indices, gsg_parent_t* out);
 GSG_API int gsg_parent_free(gsg_parent_t parent);
-/* Sample and induce `count` subgraphs (sampler k uses seed + k). 1 <= m <= n <= N, m <= 16384,
+/* Sample and induce `count` subgraphs (sampler k uses seed_k above). 1 <= m <= n <= N, m <= 16384,
  * clip >= 1. Synchronizes the context stream once (to size the induced CSR arrays). */
 GSG_API int gsg_frontier_sample(gsg_ctx_t ctx, gsg_parent_t parent, int32_t n, int32_t m,
                                 int32_t clip, uint64_t seed, int32_t count, gsg_sample_t* out);

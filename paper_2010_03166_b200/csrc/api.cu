@@ -39,19 +39,6 @@ using namespace gsg;
 
 namespace {
 
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
-
 int check_ctx(gsg_ctx_t c) { return c ? GSG_OK : fail(GSG_EINVAL, "NULL context"); }
 
 // ---- host-side CSR validation (gsg.h: gsg_subgraph_upload) ----

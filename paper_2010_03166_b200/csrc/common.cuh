@@ -31,6 +31,20 @@ int cuda_fail(cudaError_t e, const char* what);
     if (!(cond)) return ::gsg::fail(code, __VA_ARGS__);  \
   } while (0)
 
+// Makes `dev` current for the scope of an API call and restores the caller's device after.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 // Grow-only device buffer.
 struct DevBuf {
   void* ptr = nullptr;

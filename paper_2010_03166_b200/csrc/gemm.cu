@@ -910,11 +910,12 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
     if (max_s > 64) max_s = 64;
     if (max_s < 1) max_s = 1;
     if (base_tiles * 2 > units) max_s = 1;  // the grid is already at least half full: no split
-    // a narrow GEMM forked next to another (the head's dW_mlp beside dH_L) takes at most 12 K
-    // pieces: fewer SMs taken from the critical-path GEMM and a cheaper reduction (config 5
-    // 2.954 -> 2.948 ms, config 3 0.594 -> 0.590 ms; profiles/r01_gemm_side_split_cap_ab.txt)
-    if (ctx->side_ws && N <= 128 && max_s > 12) max_s = 12;
                                             // (measured: the reduction costs more than the tail)
+    // a narrow GEMM running on the side stream next to another (the head's dW_mlp beside dH_L)
+    // takes at most 12 K pieces: fewer SMs taken from the critical-path GEMM and a cheaper
+    // reduction (config 5 2.954 -> 2.948 ms, config 3 0.594 -> 0.590 ms;
+    // profiles/r01_gemm_side_split_cap_ab.txt). Serialized (not forked) GEMMs are not capped.
+    if (ctx->side_ws && ctx->stream == ctx->side && N <= 128 && max_s > 12) max_s = 12;
     double best = 1e30;
     splits = 1;
     for (int s = 1; s <= max_s; s++) {

@@ -60,7 +60,7 @@ __global__ void k_frontier(const int64_t* __restrict__ indptr, const int32_t* __
   int32_t* fdeg = fnode + m;                                       // [m]
   const int s = blockIdx.x;
   if (threadIdx.x != 0) return;
-  const uint64_t sd = seed + (uint64_t)s;
+  const uint64_t sd = mix64(mix64(seed) + (uint64_t)s);  // gsg.h: seed_k (decorrelated across calls)
   uint32_t* bits = bitmaps + (int64_t)s * words;
   int32_t* vs = vs_all + (int64_t)s * n;
   // FS_0: m distinct nodes, uniform over the non-isolated nodes (attempt counter t)
@@ -254,7 +254,7 @@ GSG_API int gsg_parent_upload(gsg_ctx_t c, int64_t N, int64_t nnz, const int64_t
   GSG_CHECK(N >= 1 && N < INT32_MAX && nnz >= 0, GSG_EINVAL, "bad parent sizes N=%lld nnz=%lld", (long long)N,
             (long long)nnz);
   GSG_CHECK(h_indptr[N] == nnz, GSG_EGRAPH, "indptr[N] != nnz");
-  cudaSetDevice(c->device);
+  DeviceGuard dg(c->device);
   std::vector<int32_t> non;
   non.reserve(N);
   for (int64_t i = 0; i < N; i++)
@@ -281,7 +281,7 @@ GSG_API int gsg_parent_upload(gsg_ctx_t c, int64_t N, int64_t nnz, const int64_t
 
 GSG_API int gsg_parent_free(gsg_parent_t p) {
   if (!p) return GSG_OK;
-  cudaSetDevice(p->device);
+  DeviceGuard dg(p->device);
   cudaFree(p->indptr);
   cudaFree(p->indices);
   cudaFree(p->noniso);
@@ -296,7 +296,7 @@ GSG_API int gsg_frontier_sample(gsg_ctx_t c, gsg_parent_t p, int32_t n, int32_t 
             "bad sampler sizes n=%d m=%d clip=%d count=%d", n, m, clip, count);
   GSG_CHECK((int64_t)n <= p->n_noniso && (int64_t)m <= p->n_noniso, GSG_EINVAL,
             "n=%d / m=%d exceed the parent's %lld non-isolated nodes", n, m, (long long)p->n_noniso);
-  cudaSetDevice(c->device);
+  DeviceGuard dg(c->device);
   cudaStream_t st = c->stream;
   const int64_t words = (p->N + 31) / 32;
   DevBuf bitmaps, vs, nv, wordpre;
@@ -383,7 +383,7 @@ GSG_API int gsg_sample_get(gsg_sample_t s, int32_t k, int32_t* n_k, int64_t* nnz
 
 GSG_API int gsg_sample_free(gsg_sample_t s) {
   if (!s) return GSG_OK;
-  cudaSetDevice(s->device);
+  DeviceGuard dg(s->device);
   cudaFree(s->nodes);
   cudaFree(s->indptr);
   cudaFree(s->indices);

@@ -552,9 +552,11 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
       if (cap > 0) {
         const int nch = a.nchunks;
         if (int rc = ctx->ws_mega.reserve(sizeof(float4) * (size_t)cap * kMegaSegs * a.f4)) return rc;
-        void* old = ctx->ws_megactr.ptr;
+        // a grown buffer is zeroed whole (cudaMalloc may hand back the old address, so growth,
+        // not a pointer change, is the test); afterwards every launch leaves the counters at zero
+        const size_t had = ctx->ws_megactr.bytes;
         if (int rc = ctx->ws_megactr.reserve(sizeof(int) * (size_t)cap * std::max(nch, 16))) return rc;
-        if (ctx->ws_megactr.ptr != old) GSG_CUDA(cudaMemsetAsync(ctx->ws_megactr.ptr, 0, ctx->ws_megactr.bytes, ctx->stream));
+        if (ctx->ws_megactr.bytes != had) GSG_CUDA(cudaMemsetAsync(ctx->ws_megactr.ptr, 0, ctx->ws_megactr.bytes, ctx->stream));
         a.mega_ws = static_cast<float4*>(ctx->ws_mega.ptr);
         a.mega_ctr = static_cast<int*>(ctx->ws_megactr.ptr);
       }

@@ -234,6 +234,29 @@ def test_oracle_frontier_pop_uniform_mutant_is_rejected(tmp_path):
 
 
 # ------------------------------------------------------------------------------ GPU
+_M64 = (1 << 64) - 1
+
+
+def _mix64(z):
+    z = (z + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def sampler_seed(seed, k):
+    """Seed of sampler k of one gsg_frontier_sample call (include/gsg.h: mix64(mix64(seed) + k))."""
+    return _mix64((_mix64(seed) + k) & _M64)
+
+
+def test_sampler_seeds_are_decorrelated():
+    """Consecutive calls do not repeat subgraphs: sampler k of seed S != sampler k-1 of seed S+1
+    (with seed + k they were identical)."""
+    keys = {sampler_seed(s, k) for s in range(50) for k in range(50)}
+    assert len(keys) == 2500
+    assert sampler_seed(7, 1) != sampler_seed(8, 0)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("cid", [1, 2, 5])
 def test_gpu_sampler_matches_oracle(cid):
@@ -247,7 +270,7 @@ def test_gpu_sampler_matches_oracle(cid):
     batch = pg.sample(cfg.n, cfg.m, seed, count=count, clip=16)
     for k in range(count):
         ip, ix, nd = batch.to_host(k)
-        v = orc.frontier_sample(p.indptr, p.indices, cfg.n, cfg.m, 16, seed + k)
+        v = orc.frontier_sample(p.indptr, p.indices, cfg.n, cfg.m, 16, sampler_seed(seed, k))
         assert np.array_equal(nd, v), f"sample {k}: node sets differ"
         rip, rix = orc.induce(p.indptr, p.indices, v)
         assert np.array_equal(ip, rip) and np.array_equal(ix, rix), f"sample {k}: induced CSR differs"
