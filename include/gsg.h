@@ -366,6 +366,20 @@ GSG_API int gsg_sample_free(gsg_sample_t s);
 GSG_API int gsg_gather_rows(gsg_ctx_t ctx, int32_t rows, int64_t row_bytes, const void* d_src,
                             int64_t src_pitch, const int32_t* d_idx, void* d_dst, int64_t dst_pitch);
 
+/* ==== measurement: the aggregation kernels' machine ceiling ================ *
+ * Not a step of the method. Random whole-row gathers from the caller's DEVICE matrix X
+ * (rows x ldx fp32, row-major, read only), the access pattern of gsg_spmm with the sparse
+ * structure removed: each warp gathers rows of row_floats columns at uniformly random row ids,
+ * 8 rows in flight, 256-bit loads; grids of 2, 3 and 4 CTAs per SM are timed with CUDA events
+ * on the context stream (one warm-up launch each) and the best gathered GB/s is returned in
+ * *gbs. With X L2-resident (<= ~half the L2) this is the L2->SM random-gather ceiling that the
+ * SpMM's effective bandwidth is reported against. Synchronizes the context stream; must not be
+ * called inside a stream capture.
+ * Errors: GSG_EINVAL (NULL, rows < 1, row_floats not a multiple of 8 in [8, 256], ldx < row_floats,
+ * ldx % 8 != 0, X not 32-byte aligned), GSG_ECUDA. */
+GSG_API int gsg_diag_gather_ceiling(gsg_ctx_t ctx, const float* d_X, int32_t rows, int64_t ldx,
+                                    int32_t row_floats, double* gbs);
+
 /* ==== data parallelism (row a9) ======================================================== */
 /* NCCL plumbing (libnccl.so.2 is resolved at run time; the process's already-loaded copy,
  * e.g. torch's, is reused). The 128-byte unique id is produced on one rank and broadcast

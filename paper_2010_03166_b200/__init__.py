@@ -82,6 +82,7 @@ _SIGS = {
     "gsg_nccl_comm_init": (_int, [_vp, _int, _int, _vp, ctypes.POINTER(_vp)]),
     "gsg_nccl_comm_destroy": (_int, [_vp]),
     "gsg_allreduce_grads": (_int, [_vp, _vp, _vp, _vp, _int, _int]),
+    "gsg_diag_gather_ceiling": (_int, [_vp, _vp, _i32, _i64, _i32, ctypes.POINTER(ctypes.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -329,6 +330,14 @@ class Context:
         assert dst.element_size() == es and src.shape[1] == dst.shape[1]
         check(gsg_gather_rows(self.h, rows, src.shape[1] * es, _ptr(src), src.stride(0) * es, idx_ptr, _ptr(dst),
                               dst.stride(0) * es))
+
+    def diag_gather_ceiling(self, X, row_floats: int | None = None) -> float:
+        """Random-row-gather GB/s from the device matrix X (gsg_diag_gather_ceiling): the measured
+        ceiling of the aggregation kernels when X is L2-resident. Synchronizes the stream."""
+        rf = min(256, X.shape[1]) if row_floats is None else row_floats
+        out = ctypes.c_double(0.0)
+        check(gsg_diag_gather_ceiling(self.h, _ptr(X), X.shape[0], _ld(X), rf, ctypes.byref(out)))
+        return out.value
 
     def spmm(self, sg: Subgraph, X, Y, transpose: bool = False, Ylp=None, mask=None, f: int | None = None,
              mask_bits=None):

@@ -421,8 +421,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
 }
 
 // Sub-warp kernel (f <= 64): groups of G lanes, one row per group; heavy rows CTA-split.
-// Rows with deg' >= kNarrowSplitDeg (the first rows of the degree-sorted order; at most two per
-// CTA) are split over all NG = 8 * 32/G lane groups of a CTA and reduced through shared memory
+// Rows with deg' >= kNarrowSplitDeg (the first rows of the degree-sorted order, whole degree
+// buckets, at most two per CTA) are split over all NG = 8 * 32/G lane groups of a CTA and reduced through shared memory
 // in group order; every other row is one group's. (At f <= 64 a row costs one dependent round
 // trip per 8 neighbors, so a 170-degree row alone would otherwise set the kernel's length.)
 constexpr int kNarrowSplitDeg = 64;
@@ -436,10 +436,20 @@ __global__ void __launch_bounds__(kThreads) k_spmm_narrow(SpmmArgs a) {
   const int warp = threadIdx.x >> 5;
   const int g = lane / G, gl = lane % G;
   const int gi = warp * PER + g;
-  if (threadIdx.x == 0) {  // at most two split rows per CTA: enough to cut the critical path of
-    int h = 0;              // a few outlier rows without serializing a batch's many medium rows
-    for (int bkt = 32 - __clz(kNarrowSplitDeg); bkt < kBins; bkt++) h += a.bucket_counts[bkt];
-    s_nh = min(h, 2 * (int)gridDim.x);
+  if (threadIdx.x == 0) {
+    // at most two split rows per CTA: enough to cut the critical path of a few outlier rows
+    // without serializing a batch's many medium rows. The split set is whole degree buckets,
+    // highest first (perm leads with them), so it depends only on the degree histogram and
+    // not on the (atomic) order of rows inside a bucket: every row's summation order is fixed
+    // and the result is bitwise reproducible (R14).
+    const int cap = 2 * (int)gridDim.x;
+    int h = 0;
+    for (int bkt = kBins - 1; bkt >= 32 - __clz(kNarrowSplitDeg); bkt--) {
+      const int c = a.bucket_counts[bkt];
+      if (h + c > cap) break;
+      h += c;
+    }
+    s_nh = h;
   }
   __syncthreads();
   const int n_split = s_nh;

@@ -26,6 +26,16 @@ def chain_order(f_in: int, f_out: int) -> int:
     return 2 if f_in > f_out else 1
 
 
+def spmm_widths(dims, order, input_grad: bool = True) -> list:
+    """Feature widths of the aggregation launches of one step, in launch order: the forward's
+    a2 per layer (f_in under order 1, f_out under order 2), then the backward's a7 from the top
+    layer down (layer 1's a7 is skipped without the input gradient under order 1)."""
+    L = len(dims) - 1
+    w = [dims[l + 1] if order[l] == 2 else dims[l] for l in range(L)]
+    back = [w[l] for l in range(L - 1, -1, -1) if l > 0 or input_grad or order[l] == 2]
+    return w + back
+
+
 def ld_for(f: int, align: int = 8) -> int:
     return (f + align - 1) // align * align
 
@@ -144,6 +154,9 @@ class GCNStep:
 
     def _hb(self, l: int, n: int):
         return None if self.Hb[l] is None else self.Hb[l][:n]
+
+    def spmm_widths(self, input_grad: bool = True) -> list:
+        return spmm_widths(self.dims, self.order, input_grad)
 
     def work_edge_features(self, nnz_hat: int, input_grad: bool = True) -> int:
         """2 * nnz' * f edge-features per layer (a2 + a7), summed over layers, where f is

@@ -29,8 +29,14 @@ def test_ours_line():
     assert d["higher_is_better"] is True and d["scaling"] == "weak" and d["data"] == "synthetic"
     assert d["config"]["workload"].startswith("config1")
     r = d["roofline"]
-    assert r["bound"] in ("hbm", "tensor", "alu") and r["achieved"] > 0 and r["peak"] > 0
+    # the SpMM's X is L2-resident: its ceiling is the L2 random-gather rate measured in the same run
+    assert r["bound"] == "l2" and r["unit"] == "GB/s" and r["achieved"] > 0 and r["peak"] > 0
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert 0 < r["frac"] <= 1.2, r["frac"]
+    assert "measured in this run" in r["peak_source"] and r["peak_by_row_bytes"]
+    hb = r["hbm"]
+    assert hb["peak"] > 0 and 0 < hb["frac"] < 1.0 and hb["min_bytes_per_step"] > 0
+    assert r["widths_per_step"] == [50, 50]
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0

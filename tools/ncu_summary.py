@@ -2,8 +2,8 @@
 
   python tools/ncu_summary.py launches <launches.csv>      per-kernel share of device time
   python tools/ncu_summary.py report <file.ncu-rep> [...]  key metrics of each captured launch
-  python tools/ncu_summary.py traffic <spmm_metrics.csv> [k]  DRAM / L2 bytes of the last k (6)
-        SpMM launches (one config-5 step) -> profiles/spmm_traffic.json (bench.py's roofline.traffic)
+  python tools/ncu_summary.py traffic <spmm_metrics.csv> [cid]  DRAM / L2 bytes of the last step's
+        SpMM launches, tagged by width -> profiles/spmm_traffic_c<cid>.json (bench.py's roofline.traffic)
 """
 import collections
 import csv
@@ -63,7 +63,29 @@ def report(path):
     return res
 
 
-def traffic(path, k=6):
+def traffic(path, cid=5):
+    """DRAM / L2 bytes of the last step's SpMM launches, each tagged with its feature width (the
+    launch order of one step, paper_2010_03166_b200.step.spmm_widths) -> the per-config file
+    bench.py reads (profiles/spmm_traffic_c<cid>.json)."""
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import workload as wl
+    from paper_2010_03166_b200.step import chain_order, spmm_widths
+    cfg = wl.CONFIGS[cid]
+    widths = spmm_widths(cfg.dims, [chain_order(cfg.dims[l], cfg.dims[l + 1]) for l in range(cfg.L)])
+    res = _traffic(path, len(widths))
+    by_width = collections.OrderedDict()
+    for x, f in zip(res["launches"], widths):
+        x["f"] = f
+        by_width.setdefault(str(f), []).append((x["dram_read"] or 0) + (x["dram_write"] or 0))
+    res["config"] = cid
+    res["widths"] = widths
+    res["dram_bytes_by_width"] = {f: sum(v) / len(v) for f, v in by_width.items()}
+    res["source"] = res["source"].replace("(one config-5 step)", f"(one config-{cid} step)")
+    return res
+
+
+def _traffic(path, k=6):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h, data = rows[hi], rows[hi + 1:]
@@ -88,7 +110,7 @@ def traffic(path, k=6):
 if __name__ == "__main__":
     mode = sys.argv[1]
     if mode == "traffic":
-        print(json.dumps(traffic(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 6), indent=1))
+        print(json.dumps(traffic(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 5), indent=1))
     elif mode == "launches":
         print(json.dumps(launches(sys.argv[2]), indent=1))
     else:
