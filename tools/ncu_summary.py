@@ -103,7 +103,7 @@ def _traffic(path, k=6):
                     "lts_bytes": m.get("lts__t_bytes.sum"), "us": m.get("gpu__time_duration.sum")})
     tot = sum((x["dram_read"] or 0) + (x["dram_write"] or 0) for x in out)
     return {"source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum over the last {k} "
-                      "k_spmm_wide launches (one config-5 step) of bench.py --steps 2 --warmup 3",
+                      "k_spmm_* launches (one config-5 step) of bench.py --steps 2 --warmup 3",
             "launches": out, "dram_bytes_per_launch": tot / len(out) if out else None}
 
 
