@@ -32,9 +32,39 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# NCCL prints a version banner on stdout at communicator init unless told otherwise; the driver
-# reads exactly one JSON line from stdout.
-os.environ.setdefault("NCCL_DEBUG", "WARN")
+# NCCL logs at INFO (communicator init: ranks, NVLink/NVLS topology, tuning tables) into a
+# per-process file, which bench.py copies to stderr after the first all-reduce and parses for
+# the JSON line (ranks seen, NVLS); stdout carries exactly the one JSON line the driver reads.
+# (the image exports NCCL_DEBUG=VERSION, so the level is set explicitly; GSG_NCCL_DEBUG overrides)
+os.environ["NCCL_DEBUG"] = os.environ.get("GSG_NCCL_DEBUG", "INFO")
+os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV,TUNING,NVLS")
+if "NCCL_DEBUG_FILE" not in os.environ:
+    import tempfile
+    os.environ["NCCL_DEBUG_FILE"] = os.path.join(tempfile.gettempdir(), f"gsg_bench_nccl.{os.getpid()}.log")
+
+
+def nccl_log_summary(echo: bool = True):
+    """Copy this process's NCCL debug log to stderr and summarize it: the communicator sizes
+    NCCL reported (nRanks), whether NVLS (NVLink SHARP in-switch reduction) was set up, and the
+    algorithm lines of the tuning output."""
+    import re
+    path = os.environ.get("NCCL_DEBUG_FILE", "")
+    if not path or "%" in path or not os.path.exists(path):
+        return {"log": None}
+    with open(path, errors="replace") as f:
+        lines = f.read().splitlines()
+    if echo:
+        for ln in lines:
+            print(ln, file=sys.stderr)
+        sys.stderr.flush()
+    nranks = sorted({int(m.group(1)) for ln in lines for m in [re.search(r"nRanks (\d+)", ln)] if m})
+    nvls = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines if "NVLS" in ln]
+    algo = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines if re.search(r"Algorithm|AllReduce \|", ln)]
+    ver = next((ln.split("NCCL version", 1)[-1].strip() for ln in lines if "NCCL version" in ln), None)
+    return {"log": path, "lines": len(lines), "version": ver, "nranks_seen": nranks,
+            "nvls_lines": nvls[:6], "nvls": any(("NVLS" in x and "enable" in x.lower()) or "multicast" in x.lower()
+                                                  for x in nvls),
+            "tuning_lines": algo[:8]}
 
 
 class stdout_to_stderr:
@@ -318,6 +348,8 @@ def main():
                          "matrix in HBM, a fresh subgraph every step")
     ap.add_argument("--sampler-pool", type=int, default=296,
                     help="subgraphs per GPU sampling call (--sampler gpu; 2 per SM keeps the latency-bound sampler busy)")
+    ap.add_argument("--nccl-timeout-ms", type=int, default=300000,
+                    help="gsg_nccl_wait time-out for the all-reduce (a stalled or dead peer aborts the run)")
     ap.add_argument("--flush-l2", action="store_true",
                     help="flush L2 (write a 2x-L2 buffer) before every step of the per-step timing pass")
     args = ap.parse_args()
@@ -454,6 +486,15 @@ def main():
         if overlap:
             stream.wait_event(ev_ar)
 
+    def wait_stream():
+        """stream.synchronize() with NCCL failure detection when a communicator exists
+        (gsg_nccl_wait: asynchronous NCCL errors and a stall time-out abort the run loudly)."""
+        if comm is not None:
+            if comm_ctx is not None:
+                comm_ctx.nccl_wait(comm, args.nccl_timeout_ms)
+            ctx.nccl_wait(comm, args.nccl_timeout_ms)
+        stream.synchronize()
+
     for i in range(2):
         step_run(i)
     stream.synchronize()
@@ -471,9 +512,30 @@ def main():
             work += step_run(i)
         drain_comm()
         ev1.record(stream)
-        stream.synchronize()
+        wait_stream()
     launches = int(round(launches_per_step * args.steps)) if graphs is not None else ctx.launch_count() - launches0
     ms = ev0.elapsed_time(ev1)
+    nccl_info = nccl_log_summary() if comm is not None else None
+    # a9 alone: K back-to-back all-reduces of the flat gradient buffer on the stream the step uses
+    ar_ms = None
+    if comm is not None:
+        ar_ctx, ar_stream = (comm_ctx, comm_stream) if overlap else (ctx, stream)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ar_stream.synchronize()
+        a0.record(ar_stream)
+        for _ in range(args.steps):
+            ar_ctx.allreduce_grads(comm, [runner.grad_flat], average=True)
+        a1.record(ar_stream)
+        ar_ctx.nccl_wait(comm, args.nccl_timeout_ms)
+        ar_ms = a0.elapsed_time(a1) / args.steps
+    per_rank = {"rank": rank, "nnz_hat": nnz_hat, "nodes": [g.n for g in pool], "ms_per_step": ms / args.steps,
+                "allreduce_ms": ar_ms, "allreduce_bytes": runner.grad_flat.numel() * 4}
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, per_rank)
+        per_rank = gathered
+    else:
+        per_rank = [per_rank]
     torch.cuda.synchronize()
     max_ms, total_work = dp.reduce_timing(ms, float(work), device=dev)
     value = total_work / (max_ms / 1e3)
@@ -772,6 +834,7 @@ def main():
                "step_ms_dist": step_dist, "training_mode": training,
                "value_noself": value_noself, "subgraphs_per_s": subgraphs_per_s,
                "layer_roofline_frac": layer_roof,
+               "per_rank": per_rank, "nccl": nccl_info,
                "setup_s": time.time() - t_setup}
         if gpu_loop is not None:
             out["gpu_sampled_loop"] = gpu_loop

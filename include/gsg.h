@@ -389,9 +389,16 @@ GSG_API int gsg_nccl_comm_init(gsg_ctx_t ctx, int nranks, int rank, const void* 
                                void** out_comm);
 GSG_API int gsg_nccl_comm_destroy(void* comm);
 /* Sum (average = 1: mean) of each buffer across the communicator's ranks, in place, on the
- * context stream: bufs[i] (device fp32) has counts[i] elements. One grouped call. */
+ * context stream: bufs[i] (device fp32) has counts[i] elements. One grouped call. Returns
+ * GSG_ENCCL without enqueueing if the communicator already holds an asynchronous error. */
 GSG_API int gsg_allreduce_grads(gsg_ctx_t ctx, void* nccl_comm, float* const* bufs,
                                 const int64_t* counts, int nbufs, int average);
+/* Failure detection for the collective: waits until everything enqueued on the context stream
+ * (e.g. gsg_allreduce_grads) has finished, polling ncclCommGetAsyncError meanwhile. Returns
+ * GSG_OK, or GSG_ENCCL if NCCL reports an asynchronous error (a peer failed) or the stream is
+ * not done after timeout_ms (> 0; <= 0 waits forever): in both cases the communicator has been
+ * aborted (ncclCommAbort) and must not be used or destroyed again. GSG_ECUDA on a CUDA fault. */
+GSG_API int gsg_nccl_wait(gsg_ctx_t ctx, void* nccl_comm, int64_t timeout_ms);
 
 #ifdef __cplusplus
 }

@@ -82,6 +82,7 @@ _SIGS = {
     "gsg_nccl_comm_init": (_int, [_vp, _int, _int, _vp, ctypes.POINTER(_vp)]),
     "gsg_nccl_comm_destroy": (_int, [_vp]),
     "gsg_allreduce_grads": (_int, [_vp, _vp, _vp, _vp, _int, _int]),
+    "gsg_nccl_wait": (_int, [_vp, _vp, _i64]),
     "gsg_diag_gather_ceiling": (_int, [_vp, _vp, _i32, _i64, _i32, ctypes.POINTER(ctypes.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -414,6 +415,11 @@ class Context:
     def wait_event(self, event):
         """Context stream waits for a torch.cuda.Event (an external-event node when capturing)."""
         check(gsg_ctx_wait_event(self.h, event.cuda_event))
+
+    def nccl_wait(self, comm: int, timeout_ms: int = 300000):
+        """Wait for this context's stream with NCCL failure detection (gsg_nccl_wait): raises
+        GsgError (and aborts the communicator) on an asynchronous NCCL error or a timeout."""
+        check(gsg_nccl_wait(self.h, comm, int(timeout_ms)))
 
     def allreduce_grads(self, comm: int, tensors, average: bool = True):
         n = len(tensors)

@@ -3,8 +3,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cstdarg>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -108,6 +110,8 @@ struct Nccl {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   bool ok = false;
 };
 
@@ -125,8 +129,10 @@ Nccl load_nccl() {
       N.GroupStart = (decltype(N.GroupStart))dlsym(h, "ncclGroupStart");
       N.GroupEnd = (decltype(N.GroupEnd))dlsym(h, "ncclGroupEnd");
       N.GetErrorString = (decltype(N.GetErrorString))dlsym(h, "ncclGetErrorString");
+      N.CommGetAsyncError = (decltype(N.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+      N.CommAbort = (decltype(N.CommAbort))dlsym(h, "ncclCommAbort");
       N.ok = N.GetUniqueId && N.CommInitRank && N.CommDestroy && N.AllReduce && N.GroupStart && N.GroupEnd &&
-             N.GetErrorString;
+             N.GetErrorString && N.CommGetAsyncError && N.CommAbort;
     }
   }
   return N;
@@ -784,6 +790,10 @@ GSG_API int gsg_allreduce_grads(gsg_ctx_t c, void* comm, float* const* bufs, con
   Nccl& N = nccl();
   GSG_CHECK(N.ok, GSG_ENCCL, "libnccl.so.2 not loadable");
   DeviceGuard dg(c->device);
+  ncclResult_t ae = ncclSuccess;  // an earlier collective failed asynchronously: report it, enqueue nothing
+  if (N.CommGetAsyncError(static_cast<ncclComm_t>(comm), &ae) == ncclSuccess && ae != ncclSuccess &&
+      ae != ncclInProgress)
+    return nccl_fail(ae, "NCCL communicator in an asynchronous error state (earlier collective)");
   ncclResult_t r = N.GroupStart();
   if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
   for (int i = 0; i < nbufs; i++) {
@@ -795,6 +805,35 @@ GSG_API int gsg_allreduce_grads(gsg_ctx_t c, void* comm, float* const* bufs, con
   r = N.GroupEnd();
   if (r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
   return GSG_OK;
+}
+
+GSG_API int gsg_nccl_wait(gsg_ctx_t c, void* comm, int64_t timeout_ms) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(comm, GSG_EINVAL, "NULL communicator");
+  Nccl& N = nccl();
+  GSG_CHECK(N.ok, GSG_ENCCL, "libnccl.so.2 not loadable");
+  DeviceGuard dg(c->device);
+  ncclComm_t cm = static_cast<ncclComm_t>(comm);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(c->stream);
+    ncclResult_t ae = ncclSuccess;
+    const ncclResult_t qr = N.CommGetAsyncError(cm, &ae);
+    if (qr != ncclSuccess) return nccl_fail(qr, "ncclCommGetAsyncError");
+    if (ae != ncclSuccess && ae != ncclInProgress) {
+      N.CommAbort(cm);
+      return nccl_fail(ae, "NCCL asynchronous error (communicator aborted)");
+    }
+    if (q == cudaSuccess) return GSG_OK;
+    if (q != cudaErrorNotReady) return cuda_fail(q, "cudaStreamQuery(gsg_nccl_wait)");
+    const int64_t ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_ms > 0 && ms > timeout_ms) {
+      N.CommAbort(cm);
+      return fail(GSG_ENCCL, "gsg_nccl_wait: stream not done after %lld ms (a peer rank stalled or died?); "
+                             "communicator aborted", (long long)ms);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
 }
 
 }  // extern "C"

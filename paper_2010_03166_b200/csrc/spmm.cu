@@ -576,6 +576,9 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
     a.w256 = w256_env && (uintptr_t)X % 32 == 0 && ldx % 8 == 0;  // GSG_SPMM_W256=0: 128-bit path (A/B)
     if (a.w256) a.cw = (a.cw + 1) & ~1;  // chunks start on 32-byte column pairs
     const int64_t tasks = (int64_t)sg->n * a.nchunks;
+    static const int minb_env = getenv("GSG_SPMM_MINB") ? atoi(getenv("GSG_SPMM_MINB")) : 0;  // A/B: force 2 or 3
+    if (minb_env == 3) return launch_k(ctx, k_spmm_wide<3>, &occ_wide3, a, tasks);
+    if (minb_env == 2) return launch_k(ctx, k_spmm_wide<2>, &occ_wide, a, tasks);
     if (tasks >= 6LL * ctx->num_sms * 3 * kWarps) return launch_k(ctx, k_spmm_wide<3>, &occ_wide3, a, tasks);
     return launch_k(ctx, k_spmm_wide<2>, &occ_wide, a, tasks);
   }

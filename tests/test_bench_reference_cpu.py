@@ -36,3 +36,21 @@ def test_reference_arm_other_ranks_exit_quietly():
               "--steps", "1", "--warmup", "3")
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.strip() == ""
+
+
+def test_nccl_log_summary(tmp_path, monkeypatch, capsys):
+    """bench.py's NCCL INFO log handling: copied to stderr (not stdout, which carries only the JSON
+    line) and summarized (ranks NCCL saw, NVLS set-up lines)."""
+    import importlib.util
+    log = tmp_path / "nccl.log"
+    log.write_text("h:1:1 [0] NCCL INFO NCCL version 2.28.9+cuda12.9\n"
+                   "h:1:1 [0] NCCL INFO comm 0x1 rank 0 nRanks 8 nNodes 1 localRanks 8 localRank 0 MNNVL 0\n"
+                   "h:1:1 [0] NCCL INFO NVLS multicast support is available on dev 0 (NVLS_NCHANNELS 16)\n")
+    monkeypatch.setenv("NCCL_DEBUG_FILE", str(log))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    s = bench.nccl_log_summary()
+    cap = capsys.readouterr()
+    assert cap.out == "" and "nRanks 8" in cap.err
+    assert s["nranks_seen"] == [8] and s["nvls"] and s["version"].startswith("2.28.9")
