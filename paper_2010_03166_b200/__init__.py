@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgsg.so")
+# GSG_LIB_PATH: load another build of the same library (A/B measurements of two builds in one run)
+LIB_PATH = os.environ.get("GSG_LIB_PATH") or os.path.join(_HERE, "libgsg.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "gsg.h")
 
 if not os.path.exists(LIB_PATH):

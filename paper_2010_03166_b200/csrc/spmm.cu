@@ -162,32 +162,35 @@ __device__ __forceinline__ void ld256(const void* p, float4 (&x)[2]) {
 // (lo = byte offset of that pair; idle lanes re-read the chunk's last pair), so a 1 KB chunk
 // row is ONE warp-wide load instruction instead of two 512-byte ones -- half the load
 // instructions and L1 requests per gathered byte, same bytes and registers in flight.
+template <int UU>
 __device__ __forceinline__ void warp_row_sum256(const SpmmArgs& a, int2* __restrict__ st, int b, int e, uint32_t lo,
                                                 int lane, Acc& A) {
+  static_assert(UU % 2 == 0 && UU <= 8, "UU: even, <= 8");
   const char* X0 = reinterpret_cast<const char*>(a.X) + lo;
 #pragma unroll
   for (int q = 0; q < 2 * V; q++) A.v[q] = make_float2(0.f, 0.f);
   for (int k0 = b; k0 < e; k0 += 32) {
     const int k = k0 + lane;
-    if (k < e) st[lane] = make_int2((int)((uint32_t)__ldg(a.col + k) * a.ldx16), __float_as_int(__ldg(a.val + k)));
+    int2 pr = make_int2(0, 0);
+    if (k < e) pr = make_int2((int)((uint32_t)__ldg(a.col + k) * a.ldx16), __float_as_int(__ldg(a.val + k)));
+    // slots past the row's end gather the group's first neighbor row again with weight 0, so the
+    // last (partial) batch is an ordinary U-wide batch: one round trip instead of one per
+    // remaining neighbor, and no predication (which made ptxas spread the gathers out)
+    const int off0 = __shfl_sync(0xffffffffu, pr.x, 0);
+    if (k >= e) pr = make_int2(off0, 0);
+    st[lane] = pr;
+    if (UU % 8 != 0 && lane < 8) st[32 + lane] = make_int2(off0, 0);  // a batch may run past slot 31
     __syncwarp();
     const int cnt = min(32, e - k0);
-    int j = 0;
-    for (; j + U <= cnt; j += U) {
-      int4 p[U / 2];
+    for (int j = 0; j < cnt; j += UU) {
+      int4 p[UU / 2];
 #pragma unroll
-      for (int q = 0; q < U / 2; q++) p[q] = reinterpret_cast<const int4*>(st)[(j >> 1) + q];
-      float4 x[U][V];
+      for (int q = 0; q < UU / 2; q++) p[q] = reinterpret_cast<const int4*>(st)[(j >> 1) + q];
+      float4 x[UU][V];
 #pragma unroll
-      for (int u = 0; u < U; u++) ld256(X0 + ((u & 1) ? (uint32_t)p[u >> 1].z : (uint32_t)p[u >> 1].x), x[u]);
+      for (int u = 0; u < UU; u++) ld256(X0 + ((u & 1) ? (uint32_t)p[u >> 1].z : (uint32_t)p[u >> 1].x), x[u]);
 #pragma unroll
-      for (int u = 0; u < U; u++) acc_fma(A, __int_as_float((u & 1) ? p[u >> 1].w : p[u >> 1].y), x[u]);
-    }
-    for (; j < cnt; j++) {
-      const int2 p = st[j];
-      float4 x[V];
-      ld256(X0 + (uint32_t)p.x, x);
-      acc_fma(A, __int_as_float(p.y), x);
+      for (int u = 0; u < UU; u++) acc_fma(A, __int_as_float((u & 1) ? p[u >> 1].w : p[u >> 1].y), x[u]);
     }
     __syncwarp();
   }
@@ -280,9 +283,9 @@ __device__ __forceinline__ float4 acc_part(const Acc& A, int q) {
 // gathers in flight on large problems (config 5 2.973 -> 2.945 ms, config 3 0.619 -> 0.594 ms);
 // 2 (128 registers) wins when a warp gets fewer than ~6 light tasks (config 2 SpMM 35 vs 39 µs,
 // config 1). profiles/r01_spmm_occupancy_ab.txt.
-template <int MINB>
+template <int MINB, bool W256, int UU = U>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
-  __shared__ __align__(16) int2 stage[kWarps][32];
+  __shared__ __align__(16) int2 stage[kWarps][40];
   __shared__ float4 part[kWarps][32 * V];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -322,10 +325,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
     const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
     int c4, c4b;  // output float4 columns of acc_part(A, 0) and acc_part(A, 1)
     Acc A;
-    if (a.w256) {
+    if (W256) {
       c4 = c0 + 2 * lane;
       c4b = c4 + 1;
-      warp_row_sum256(a, st, w0, w1, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
+      warp_row_sum256<UU>(a, st, w0, w1, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
     } else {
       c4 = c0 + lane;
       c4b = c4 + 32;
@@ -398,15 +401,15 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
     uint32_t mw0 = 0, mw1 = 0;
     if (a.mbits) {
       const uint32_t* mr = a.mbits + (int64_t)row * a.ldmb;
-      const int g0 = a.w256 ? c0 + 2 * lane : c0 + lane;
+      const int g0 = W256 ? c0 + 2 * lane : c0 + lane;
       if (g0 < lim) mw0 = __ldg(mr + (g0 >> 3));
-      if (!a.w256 && g0 + 32 < lim) mw1 = __ldg(mr + ((g0 + 32) >> 3));
+      if (!W256 && g0 + 32 < lim) mw1 = __ldg(mr + ((g0 + 32) >> 3));
     }
     Acc A;
-    if (a.w256) {
+    if (W256) {
       c4 = c0 + 2 * lane;
       c4b = c4 + 1;
-      warp_row_sum256(a, st, b, e, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
+      warp_row_sum256<UU>(a, st, b, e, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
     } else {
       c4 = c0 + lane;
       c4b = c4 + 32;
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
         warp_row_sum<false>(a, st, b, e, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
     }
     if (c4 < lim) store_row(a, row, c4, acc_part(A, 0), &mw0);
-    if (c4b < lim) store_row(a, row, c4b, acc_part(A, 1), a.w256 ? &mw0 : &mw1);
+    if (c4b < lim) store_row(a, row, c4b, acc_part(A, 1), W256 ? &mw0 : &mw1);
   }
 }
 
@@ -553,7 +556,7 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
   a.n_heavy_ptr = sg->counters + kBins;
   a.bucket_counts = sg->counters;
   a.n_mega_ptr = sg->counters + kNMega;
-  static std::atomic<int> occ_wide{0}, occ_wide3{0}, occ16{0}, occ8{0}, occ4{0};
+  static std::atomic<int> occ_wide{0}, occ_wide3{0}, occ_widen{0}, occ_wide3n{0}, occ16{0}, occ8{0}, occ4{0};
   if (a.f4 > 16) {
     a.nchunks = (a.f4 + 32 * V - 1) / (32 * V);
     {  // mega-row workspace: at most nnz' / kMegaMinDeg rows can have deg' >= kMegaMinDeg
@@ -577,10 +580,19 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
     if (a.w256) a.cw = (a.cw + 1) & ~1;  // chunks start on 32-byte column pairs
     const int64_t tasks = (int64_t)sg->n * a.nchunks;
     static const int minb_env = getenv("GSG_SPMM_MINB") ? atoi(getenv("GSG_SPMM_MINB")) : 0;  // A/B: force 2 or 3
-    if (minb_env == 3) return launch_k(ctx, k_spmm_wide<3>, &occ_wide3, a, tasks);
-    if (minb_env == 2) return launch_k(ctx, k_spmm_wide<2>, &occ_wide, a, tasks);
-    if (tasks >= 6LL * ctx->num_sms * 3 * kWarps) return launch_k(ctx, k_spmm_wide<3>, &occ_wide3, a, tasks);
-    return launch_k(ctx, k_spmm_wide<2>, &occ_wide, a, tasks);
+    // three CTAs per SM from ~4 (row, chunk) tasks per warp on: config 5 / 4 f = 200 (20000 / 16000
+    // tasks) 125.5 -> 119.9 / 52.6 -> 50.8 us; config 3 f = 200 (12000 tasks) stays at two
+    // (35.8 vs 38.4 us); profiles/r02_spmm_variants_ab.txt
+    const bool three = minb_env == 3 || (minb_env != 2 && tasks >= 4LL * ctx->num_sms * 3 * kWarps);
+    static const int u_env = getenv("GSG_SPMM_U") ? atoi(getenv("GSG_SPMM_U")) : 8;  // A/B: gathers in flight
+    static std::atomic<int> occ36{0}, occ44{0};
+    if (a.w256 && minb_env == 4) return launch_k(ctx, k_spmm_wide<4, true, 4>, &occ44, a, tasks);
+    if (a.w256 && three && u_env == 6) return launch_k(ctx, k_spmm_wide<3, true, 6>, &occ36, a, tasks);
+    if (a.w256)
+      return three ? launch_k(ctx, k_spmm_wide<3, true>, &occ_wide3, a, tasks)
+                   : launch_k(ctx, k_spmm_wide<2, true>, &occ_wide, a, tasks);
+    return three ? launch_k(ctx, k_spmm_wide<3, false>, &occ_wide3n, a, tasks)
+                 : launch_k(ctx, k_spmm_wide<2, false>, &occ_widen, a, tasks);
   }
   a.nchunks = 1;
   a.cw = a.f4;
