@@ -1,6 +1,6 @@
 """Measurement tool: one gsg_gemm shape, ITERS calls captured in a CUDA graph and replayed (device
 time per call without host launch gaps; GRAPH=0 launches eagerly, e.g. under ncu).
-SHAPE = "M,N,K,transA,transB", PREC = tf32 | bf16, EPI = none | relu | mask."""
+SHAPE = "M,N,K,transA,transB", PREC = tf32 | bf16, EPI = none | relu | relubits | mask | maskbits."""
 import os
 import sys
 
@@ -28,6 +28,12 @@ def main():
     elif epi == "mask":
         kw["epilogue"] = gsg.GSG_EPI_MASK
         kw["aux"] = pad(M, N, torch.float32)
+    elif epi == "maskbits":  # ReLU' gate from a bitmask (as the step's dH_L GEMM)
+        kw["epilogue"] = gsg.GSG_EPI_MASK
+        kw["aux_bits"] = torch.randint(-2**31, 2**31 - 1, (M, (N + 31) // 32), dtype=torch.int32, device="cuda")
+    elif epi == "relubits":  # ReLU epilogue that also writes the bitmask (as the step's forward GEMMs)
+        kw["epilogue"] = gsg.GSG_EPI_RELU
+        kw["C_bits"] = torch.zeros((M, (N + 31) // 32), dtype=torch.int32, device="cuda")
     stream = torch.cuda.Stream()
     ctx = gsg.Context(0, stream)
     graph = os.environ.get("GRAPH", "1") == "1"
