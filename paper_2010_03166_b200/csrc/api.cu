@@ -237,6 +237,7 @@ GSG_API int gsg_ctx_destroy(gsg_ctx_t c) {
   c->ws_splitk.release(); c->ws_splitk_side.release(); c->ws_T.release(); c->ws_dZ.release();
   c->ws_lp0.release(); c->ws_lp1.release(); c->ws_lp2.release(); c->ws_loss.release();
   c->ws_mega.release(); c->ws_megactr.release();
+  for (int i = 0; i < 2; i++) { c->ws_x3[i].release(); c->ws_x3_side[i].release(); }
   for (auto& r : c->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->prof.free_ev) cudaEventDestroy(e);
   if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
@@ -659,7 +660,8 @@ GSG_API int gsg_sage_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32
                              float* H, int64_t ldh, int precision, int flags) {
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
-  GSG_CHECK(precision == GSG_PREC_TF32, GSG_EUNSUPPORTED, "GraphSAGE layer: TF32 only");
+  GSG_CHECK(precision == GSG_PREC_TF32 || precision == GSG_PREC_FP32X3, GSG_EUNSUPPORTED,
+            "GraphSAGE layer: TF32 or FP32X3 only");
   GSG_CHECK(f_in >= 1 && fh >= 1 && fh % 4 == 0, GSG_EINVAL, "f_in=%d f_half=%d (f_half %% 4 == 0 required)", f_in, fh);
   GSG_CHECK(X && Ws && Wn && P && H && ldh >= 2 * fh, GSG_EINVAL, "NULL argument or ldh < 2 f_half");
   DeviceGuard dg(c->device);
@@ -679,7 +681,8 @@ GSG_API int gsg_sage_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
                               int precision, int flags) {
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
-  GSG_CHECK(precision == GSG_PREC_TF32, GSG_EUNSUPPORTED, "GraphSAGE layer: TF32 only");
+  GSG_CHECK(precision == GSG_PREC_TF32 || precision == GSG_PREC_FP32X3, GSG_EUNSUPPORTED,
+            "GraphSAGE layer: TF32 or FP32X3 only");
   GSG_CHECK(f_in >= 1 && fh >= 1 && fh % 4 == 0, GSG_EINVAL, "f_in=%d f_half=%d (f_half %% 4 == 0 required)", f_in, fh);
   GSG_CHECK(X && P && dH && Ws && Wn && dWs && dWn, GSG_EINVAL, "NULL argument");
   GSG_CHECK((flags & GSG_DH_PREMASKED) || H, GSG_EINVAL, "H is needed unless GSG_DH_PREMASKED");
@@ -726,24 +729,25 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
   GSG_CHECK(n >= 1 && f >= 1 && C >= 1, GSG_EINVAL, "bad head sizes n=%d f=%d C=%d", n, f, C);
   GSG_CHECK(HL && Wm && labels && S && dS && dWm && dHL && loss, GSG_EINVAL, "NULL head argument");
   GSG_CHECK(lds >= C && lds % 4 == 0, GSG_EINVAL, "lds must be >= C and a multiple of 4");
-  (void)precision;  // the head runs in TF32: H_L is fp32 and C is small (SUPPORT)
+  // the head runs in TF32 (H_L is fp32, C is small; SUPPORT), or 3xTF32 when asked
+  const int hp = precision == GSG_PREC_FP32X3 ? GSG_PREC_FP32X3 : GSG_PREC_TF32;
   DeviceGuard dg(c->device);
   RowTag rt(c, GSG_K_A8);
-  int rc = gemm_launch(c, n, C, f, HL, ldh, 0, Wm, ldw, 0, S, lds, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
+  int rc = gemm_launch(c, n, C, f, HL, ldh, 0, Wm, ldw, 0, S, lds, nullptr, 0, hp, GSG_EPI_NONE, nullptr, 0, 0, 0);
   if (rc) return rc;
   if ((rc = head_loss_launch(c, n, C, kind, S, lds, labels, node_w, dS, loss))) return rc;
   // dW_mlp = H_Lᵀ dS and dH_L = (dS W_mlpᵀ) ⊙ 1[H_L > 0] only share read-only inputs: the first
   // runs on the side stream (fork / join, as in gsg_layer_backward; serialized while profiling)
   SideFork fk(c, fork_enabled() && !c->prof.on);
   c->side_ws = true;
-  rc = gemm_launch(c, f, C, n, HL, ldh, 1, dS, lds, 0, dWm, lddw, nullptr, 0, GSG_PREC_TF32, GSG_EPI_NONE, nullptr, 0, 0, 0);
+  rc = gemm_launch(c, f, C, n, HL, ldh, 1, dS, lds, 0, dWm, lddw, nullptr, 0, hp, GSG_EPI_NONE, nullptr, 0, 0, 0);
   c->side_ws = false;
   fk.back();
   if (rc) return rc;
   BitsIO gb;  // ReLU' gate of H_L: its bitmask when given
   gb.in = HLbits;
   gb.ldi = ldhlb;
-  return gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, GSG_PREC_TF32, GSG_EPI_MASK, HL, ldh,
+  return gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, hp, GSG_EPI_MASK, HL, ldh,
                      0, 0, gb);  // fk joins on exit
 }
 

@@ -99,6 +99,8 @@ struct gsg_ctx {
   gsg::DevBuf ws_lp1;      // bf16 scratch (dZ copy / T copy)
   gsg::DevBuf ws_lp2;      // bf16 scratch
   gsg::DevBuf ws_loss;     // per-block loss partials
+  gsg::DevBuf ws_x3[2];    // GSG_PREC_FP32X3 split operand copies (A3, B3), context stream
+  gsg::DevBuf ws_x3_side[2];  // the same for the GEMMs that may be forked onto the side stream
   gsg::DevBuf ws_mega;     // SpMM mega-row segment partials
   gsg::DevBuf ws_megactr;  // SpMM mega-row (row, chunk) arrival counters, zero between launches
   cudaStream_t side = nullptr;       // fork/join side stream (layer backward: dW next to T -> dX)

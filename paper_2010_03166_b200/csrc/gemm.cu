@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -630,8 +631,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // Epilogue of one reduced float4 (columns c .. c+3 of row; w = valid columns).
+// With a ReLU bitmask output (FP32X3 splits only) the 4 columns' bits are OR-ed into their word,
+// which the GEMM's tile epilogue zeroed (OR commutes: the result does not depend on the order).
 __device__ __forceinline__ void reduce_store4(const GemmArgs& g, int row, int c, int w, const float (&x)[4]) {
   float* dst = g.C + (int64_t)row * g.ldc + c;
+  uint32_t nib = 0;
   for (int j = 0; j < w; j++) {
     float y = x[j];
     if (g.accumulate) y += dst[j];
@@ -640,7 +644,9 @@ __device__ __forceinline__ void reduce_store4(const GemmArgs& g, int row, int c,
     else if (g.epi == GSG_EPI_MASK) y = g.aux[(int64_t)row * g.ldaux + c + j] > 0.f ? y : 0.f;
     dst[j] = y;
     if (g.Clp) g.Clp[(int64_t)row * g.ldclp + c + j] = __float2bfloat16_rn(y);
+    nib |= (y > 0.f ? 1u : 0u) << j;
   }
+  if (g.cbits && nib) atomicOr(g.cbits + (int64_t)row * g.ldcb + (c >> 5), nib << (c & 31));
 }
 
 // C = epi(sum_s ws[s]) in a fixed split order (deterministic split-K reduction), one thread per
@@ -736,6 +742,29 @@ __global__ void k_to_bf16_v4(int rows, int cols4, const float4* __restrict__ src
     p.x = *reinterpret_cast<uint32_t*>(&lo);
     p.y = *reinterpret_cast<uint32_t*>(&hi);
     dst[(int64_t)r * ldd4 + c] = p;
+  }
+}
+
+// GSG_PREC_FP32X3 operand split: x = hi + lo, hi = tf32 round-to-nearest of x (an fp32 with the
+// low 13 mantissa bits zero, read exactly by kind::tf32), lo = x - hi (exact in fp32). The three
+// copies c0, c1, c2 (each hi or lo per `pat`, bit j = 1 -> copy j is lo) are stacked along K:
+// along the columns of a K-major operand (dst row r = [c0 | c1 | c2], K columns each) or along
+// the rows of an MN-major one (dst rows [c0 ; c1 ; c2], K rows each).
+__global__ void k_split3(int rows, int cols, const float* __restrict__ src, int64_t lds, float* __restrict__ dst,
+                         int64_t ldd, int along_cols, int K, int pat) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / cols), c = (int)(i % cols);
+    const float x = src[(int64_t)r * lds + c];
+    uint32_t hb;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+    const float hi = __uint_as_float(hb), lo = x - hi;
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+      const float v = (pat >> j) & 1 ? lo : hi;
+      if (along_cols) dst[(int64_t)r * ldd + (int64_t)j * K + c] = v;
+      else dst[((int64_t)j * K + r) * ldd + c] = v;
+    }
   }
 }
 
@@ -841,10 +870,27 @@ int dispatch_major(gsg_ctx* ctx, bool a_mn, bool b_mn, const CUtensorMap& ma, co
 
 }  // namespace
 
+namespace {
+int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA, const void* B,
+                     int64_t ldb, int transB, float* Cp, int64_t ldc, void* Clp, int64_t ldclp, int precision,
+                     int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate, const BitsIO& bits,
+                     bool x3);
+}  // namespace
+
 int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
                 int transB, float* Cp, int64_t ldc, void* Clp, int64_t ldclp, int precision, int epilogue,
                 const float* aux, int64_t ldaux, int split_k, int accumulate, const BitsIO& bits) {
-  GSG_CHECK(precision == GSG_PREC_TF32 || precision == GSG_PREC_BF16, GSG_EINVAL, "bad precision %d", precision);
+  return gemm_launch_impl(ctx, M, N, K, A, lda, transA, B, ldb, transB, Cp, ldc, Clp, ldclp, precision, epilogue, aux,
+                          ldaux, split_k, accumulate, bits, false);
+}
+
+namespace {
+int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA, const void* B,
+                     int64_t ldb, int transB, float* Cp, int64_t ldc, void* Clp, int64_t ldclp, int precision,
+                     int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate, const BitsIO& bits,
+                     bool x3) {
+  GSG_CHECK(precision == GSG_PREC_TF32 || precision == GSG_PREC_BF16 || precision == GSG_PREC_FP32X3, GSG_EINVAL,
+            "bad precision %d", precision);
   GSG_CHECK(epilogue >= GSG_EPI_NONE && epilogue <= GSG_EPI_MASK, GSG_EINVAL, "bad epilogue %d", epilogue);
   GSG_CHECK(M >= 0 && N >= 0 && K >= 0, GSG_EINVAL, "negative GEMM dims");
   GSG_CHECK(!accumulate || epilogue == GSG_EPI_NONE, GSG_EINVAL, "accumulate only with GSG_EPI_NONE");
@@ -861,6 +907,37 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
             "bitmask gate needs GSG_EPI_MASK and ldauxb >= ceil(N/32) (ldauxb=%lld)", (long long)bits.ldi);
   GSG_CHECK(!bits.out || (epilogue == GSG_EPI_RELU && bits.ldo >= nwords && (uintptr_t)bits.out % 4 == 0), GSG_EINVAL,
             "bitmask output needs GSG_EPI_RELU and ldcb >= ceil(N/32) (ldcb=%lld)", (long long)bits.ldo);
+  if (precision == GSG_PREC_FP32X3 && K > 0) {
+    // 3xTF32: one TF32 GEMM over K' = 3K on split copies [Ahi | Ahi | Alo] x [Bhi ; Blo ; Bhi]
+    GSG_CHECK(A && B, GSG_EINVAL, "A and B must be non-NULL");
+    GSG_CHECK(3LL * K < (int64_t)INT32_MAX, GSG_EUNSUPPORTED, "FP32X3 needs 3K < 2^31 (K=%d)", K);
+    const int64_t K3 = 3LL * K;
+    // stored shapes: A is (transA ? K x M : M x K), B is (transB ? N x K : K x N)
+    const int64_t ar = transA ? K : M, ac = transA ? M : K, br = transB ? N : K, bc = transB ? K : N;
+    GSG_CHECK(lda >= ac && ldb >= bc, GSG_EINVAL, "lda / ldb below the stored widths");
+    const int64_t lda3 = transA ? (M + 3) / 4 * 4 : (K3 + 3) / 4 * 4;  // K-major: K' along columns
+    const int64_t ldb3 = transB ? (K3 + 3) / 4 * 4 : (N + 3) / 4 * 4;
+    const int64_t a3 = transA ? K3 * lda3 : (int64_t)M * lda3, b3 = transB ? (int64_t)N * ldb3 : K3 * ldb3;
+    DevBuf* ws = ctx->side_ws ? ctx->ws_x3_side : ctx->ws_x3;
+    if (int rc = ws[0].reserve(sizeof(float) * a3)) return rc;
+    if (int rc = ws[1].reserve(sizeof(float) * b3)) return rc;
+    float* A3 = static_cast<float*>(ws[0].ptr);
+    float* B3 = static_cast<float*>(ws[1].ptr);
+    auto grid_for = [&](int64_t n) {
+      int64_t gd = (n + 255) / 256;
+      return (int)std::min<int64_t>(std::max<int64_t>(gd, 1), (int64_t)ctx->num_sms * 8);
+    };
+    // A: hi, hi, lo (pattern 0b100); B: hi, lo, hi (0b010)
+    k_split3<<<grid_for(ar * ac), 256, 0, ctx->stream>>>((int)ar, (int)ac, static_cast<const float*>(A), lda, A3, lda3,
+                                                        transA ? 0 : 1, K, 4);
+    k_split3<<<grid_for(br * bc), 256, 0, ctx->stream>>>((int)br, (int)bc, static_cast<const float*>(B), ldb, B3, ldb3,
+                                                        transB ? 1 : 0, K, 2);
+    count_launch(ctx, 2);
+    GSG_CUDA(cudaGetLastError());
+    return gemm_launch_impl(ctx, M, N, (int)K3, A3, lda3, transA, B3, ldb3, transB, Cp, ldc, Clp, ldclp,
+                            GSG_PREC_TF32, epilogue, aux, ldaux, split_k, accumulate, bits, true);
+  }
+  if (precision == GSG_PREC_FP32X3) precision = GSG_PREC_TF32;  // K = 0: the epilogue of zero
   const bool bf16 = precision == GSG_PREC_BF16;
   ProfScope ps(ctx, GSG_K_GEMM,
                (double)(bf16 ? 2 : 4) * ((double)M * K + (double)K * N) + 4.0 * M * N, 2.0 * M * N * K);
@@ -911,11 +988,13 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
     if (max_s < 1) max_s = 1;
     if (base_tiles * 2 > units) max_s = 1;  // the grid is already at least half full: no split
                                             // (measured: the reduction costs more than the tail)
-    // a narrow GEMM running on the side stream next to another (the head's dW_mlp beside dH_L)
+    // a narrow forkable GEMM (the head's dW_mlp, which runs on the side stream beside dH_L)
     // takes at most 12 K pieces: fewer SMs taken from the critical-path GEMM and a cheaper
     // reduction (config 5 2.954 -> 2.948 ms, config 3 0.594 -> 0.590 ms;
-    // profiles/r01_gemm_side_split_cap_ab.txt). Serialized (not forked) GEMMs are not capped.
-    if (ctx->side_ws && ctx->stream == ctx->side && N <= 128 && max_s > 12) max_s = 12;
+    // profiles/r01_gemm_side_split_cap_ab.txt). The cap applies to every forkable GEMM, forked
+    // or serialized (GSG_BWD_FORK=0, profiling), so both pick the same split and workspace: a
+    // serialized pass captured into a CUDA graph never has to grow the workspace.
+    if (ctx->side_ws && N <= 128 && max_s > 12) max_s = 12;
     double best = 1e30;
     splits = 1;
     for (int s = 1; s <= max_s; s++) {
@@ -925,7 +1004,14 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
       if (t < best * 0.97) { best = t; splits = s; }
     }
   }
-  if (bits.out) splits = 1;  // the bitmask is written by the tile epilogue, not the split-K reduction
+  // GSG_PREC_FP32X3 (K here is the tripled K'): at most 32 k-blocks (K' = 1024) per automatic
+  // split -- the fp32 sum inside one tensor-core accumulator drifts with the piece length
+  // (max-normalized 1.5e-5 at K' = 3600, 4.9e-5 at 12000, measured), past the 1e-5 the split
+  // precision is for; the pieces are summed by the fixed-order reduction in fp32, which also
+  // writes the ReLU bitmask then
+  if (split_k <= 0 && x3 && splits < (g.num_kb + 31) / 32) splits = (g.num_kb + 31) / 32;
+  // TF32 / BF16: the bitmask is written by the tile epilogue, not the split-K reduction
+  if (bits.out && !x3) splits = 1;
   if (splits > g.num_kb) splits = g.num_kb;
   g.kb_per_split = (g.num_kb + splits - 1) / splits;
   g.splits = (g.num_kb + g.kb_per_split - 1) / g.kb_per_split;  // no empty split
@@ -993,6 +1079,8 @@ int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, i
   }
   return GSG_OK;
 }
+
+}  // namespace
 
 int to_bf16_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t lds, void* dst, int64_t ldd) {
   GSG_CHECK(rows >= 0 && cols >= 0 && lds >= cols && ldd >= cols, GSG_EINVAL, "bad to_bf16 shape");

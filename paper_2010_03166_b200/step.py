@@ -17,7 +17,7 @@ from __future__ import annotations
 import torch
 
 from . import (GSG_DH_PREMASKED, GSG_HEAD_SIGMOID, GSG_HEAD_SOFTMAX, GSG_NORM_ROW_SELF, GSG_ORDER_A_XW,
-               GSG_PREC_BF16, GSG_PREC_TF32, GSG_W_BF16, Context, Subgraph)
+               GSG_PREC_BF16, GSG_PREC_FP32X3, GSG_PREC_TF32, GSG_W_BF16, Context, Subgraph)
 
 
 def chain_order(f_in: int, f_out: int) -> int:
@@ -54,7 +54,7 @@ class GCNStep:
         self.order = [chain_order(dims[l], dims[l + 1]) if order == "auto" else int(order) for l in range(self.L)]
         self.head = head
         self.C = classes
-        self.prec = GSG_PREC_BF16 if precision == "bf16" else GSG_PREC_TF32
+        self.prec = {"bf16": GSG_PREC_BF16, "fp32x3": GSG_PREC_FP32X3, "tf32": GSG_PREC_TF32}[precision]
         dev = torch.device("cuda", device)
         bf = self.prec == GSG_PREC_BF16
         self.W = [padded(dims[l], dims[l + 1], device=dev) for l in range(self.L)]
@@ -128,7 +128,8 @@ class GCNStep:
         if self.head != "none":
             kind = GSG_HEAD_SOFTMAX if self.head == "softmax" else GSG_HEAD_SIGMOID
             ctx.head(h, self.Wm, labels, self.S[:n], self.dS[:n], self.dWm, self.dHL[:n], n, d[-1], self.C, kind,
-                     self.loss, dHlp=None if self.dHLlp is None else self.dHLlp[:n], HL_bits=self._hb(self.L - 1, n))
+                     self.loss, dHlp=None if self.dHLlp is None else self.dHLlp[:n], precision=self.prec,
+                     HL_bits=self._hb(self.L - 1, n))
             dH, dHlp, flags = self.dHL[:n], (None if self.dHLlp is None else self.dHLlp[:n]), GSG_DH_PREMASKED
         else:
             dH, dHlp, flags = dH_top, None, 0

@@ -4,7 +4,7 @@ sampled outputs (rows / columns the oracle computes one by one), stage-isolated:
 
   a1  Â structure bit-exact, values within one fp32 rounding, valT = Alg. 4(val) bit-exact
   a2  P_l rows (random + the heaviest rows)                   <= 1e-5  (fp32 SpMM)
-  a3  H_l rows from the GPU's P_l                              <= 5e-3  (TF32/BF16 GEMM)
+  a3  H_l rows from the GPU's P_l                              <= 5e-3  (TF32/BF16 GEMM; 1e-5 FP32X3)
   a5  dW_l columns from the GPU's P_l and dZ_l                 <= 5e-3
   a6+a7  dX_l rows = Âᵀ(dZ_l W_lᵀ) ⊙ gate, oracle T from GPU dZ <= 5e-3 (after a tensor-core GEMM)
   a8  head loss / dS rows from the GPU's S                     <= 1e-5 relative
@@ -22,6 +22,11 @@ from paper_2010_03166_b200.step import GCNStep
 pytestmark = pytest.mark.gpu
 
 SPMM_TOL, GEMM_TOL = 1e-5, 5e-3
+X3_TOL = 1e-5   # GSG_PREC_FP32X3 (configs 1-2, "fp32"): GEMM stages graded at the fp32 tolerance
+
+
+def gemm_tol(cfg):
+    return X3_TOL if cfg.precision == "fp32x3" else GEMM_TOL
 
 
 def rel(gpu, ref):
@@ -64,6 +69,7 @@ def run_config(ctx, cid):
 def test_config_step_sampled_parity(ctx, cid):
     cfg, g, inp, sg, step, X, labels, dH_top = run_config(ctx, cid)
     n, L, d = g.n, cfg.L, cfg.dims
+    GT = gemm_tol(cfg)
     A = orc.normalize(g.indptr, g.indices, orc.NORM_ROW_SELF)
     # a1
     ip, ix, v, vt = sg.download()
@@ -80,7 +86,7 @@ def test_config_step_sampled_parity(ctx, cid):
             # chain order 2 (§7.1): Y = X W (GEMM), H = ReLU(Â Y) (SpMM)
             Y = h(step.P[l][:n])
             Wl = inp.Ws[l].astype(np.float64)
-            assert rel(Y[rows], orc.gemm(X_in[rows], Wl)) <= GEMM_TOL, f"layer {l} Y"
+            assert rel(Y[rows], orc.gemm(X_in[rows], Wl)) <= GT, f"layer {l} Y"
             Href = np.stack([np.maximum(orc.spmm(A, Y, int(i), int(i) + 1)[i], 0) for i in rows])
             assert rel(h(step.H[l][:n])[rows], Href) <= SPMM_TOL, f"layer {l} H (order 2)"
             continue
@@ -92,7 +98,7 @@ def test_config_step_sampled_parity(ctx, cid):
         Pin = h(step.Plp[l][:n]) if bf else P
         Wl = inp.Ws[l].astype(np.float64)
         Href = np.maximum(orc.gemm(Pin[rows], Wl), 0)
-        assert rel(h(step.H[l][:n])[rows], Href) <= GEMM_TOL, f"layer {l} H"
+        assert rel(h(step.H[l][:n])[rows], Href) <= GT, f"layer {l} H"
     # backward: the gate applied to layer L's upstream gradient
     if cfg.head != "none":
         S = h(step.S[:n])
@@ -102,11 +108,11 @@ def test_config_step_sampled_parity(ctx, cid):
         assert rel(h(step.dS[:n])[rows], dS[rows]) <= 1e-5
         dSg = h(step.dS[:n])
         cols = rng.choice(cfg.classes, min(8, cfg.classes), replace=False)
-        assert rel(h(step.dWm)[:, cols], orc.gemm(HL, dSg[:, cols], transA=True)) <= GEMM_TOL
+        assert rel(h(step.dWm)[:, cols], orc.gemm(HL, dSg[:, cols], transA=True)) <= GT
         dZ_top = h(step.dHL[:n])
         Wm = inp.W_mlp.astype(np.float64)
         ref = np.where(HL[rows] > 0, orc.gemm(dSg[rows], Wm, transB=True), 0)
-        assert rel(dZ_top[rows], ref) <= GEMM_TOL
+        assert rel(dZ_top[rows], ref) <= GT
     else:
         dZ_top = np.where(h(step.H[L - 1][:n]) > 0, inp.dH.astype(np.float64), 0.0)
     dZ = dZ_top
@@ -120,7 +126,7 @@ def test_config_step_sampled_parity(ctx, cid):
         if bf:  # the BF16 GEMMs read bf16 copies of dZ
             dZin = torch.from_numpy(dZ.astype(np.float32)).bfloat16().double().numpy()
         cols = rng.choice(d[l + 1], 16, replace=False)
-        assert rel(h(step.dW[l])[:, cols], orc.gemm(P, dZin[:, cols], transA=True)) <= GEMM_TOL, f"layer {l} dW"
+        assert rel(h(step.dW[l])[:, cols], orc.gemm(P, dZin[:, cols], transA=True)) <= GT, f"layer {l} dW"
         # a6 + a7: dX = Âᵀ (dZ Wᵀ) ⊙ 1[H_{l-1} > 0] on sampled rows (scatter definition restricted
         # to the sampled output rows: dX[j] = sum over stored (i, j, a) of a * T[i])
         Wl = inp.Ws[l].astype(np.float64)
@@ -136,7 +142,7 @@ def test_config_step_sampled_parity(ctx, cid):
         if l > 0:
             ref = np.where(h(step.H[l - 1][:n])[xrows] > 0, ref, 0.0)
         dX = h(step.dX[l][:n])
-        assert rel(dX[xrows], ref) <= GEMM_TOL, f"layer {l} dX"
+        assert rel(dX[xrows], ref) <= GT, f"layer {l} dX"
         dZ = dX  # premasked dZ of the layer below (the GPU's own)
 
 

@@ -167,7 +167,7 @@ class Config:
     n: int                # subgraph node budget
     m: int                # frontier size
     dims: list            # [f0, f1, ..., fL]
-    precision: str        # "tf32" | "bf16"
+    precision: str        # "tf32" | "bf16" | "fp32x3" (3xTF32: fp32-accurate GEMMs, configs 1-2 "fp32")
     head: str             # "none" | "softmax" | "sigmoid"
     classes: int = 0
     label_p: float = 0.05
@@ -188,8 +188,8 @@ class Config:
 
 
 CONFIGS = {
-    1: Config(1, "ppi-like", 20_000, 15.0, 2.1, 0.0, 2_000, 200, [50, 128], "tf32", "none"),
-    2: Config(2, "reddit-like", 230_000, 50.0, 2.1, 1250.0, 8_000, 1000, [602, 512, 512], "tf32", "softmax", 41),
+    1: Config(1, "ppi-like", 20_000, 15.0, 2.1, 0.0, 2_000, 200, [50, 128], "fp32x3", "none"),
+    2: Config(2, "reddit-like", 230_000, 50.0, 2.1, 1250.0, 8_000, 1000, [602, 512, 512], "fp32x3", "softmax", 41),
     3: Config(3, "yelp-like", 720_000, 10.0, 2.1, 0.0, 12_000, 1000, [300, 512, 512, 512], "tf32", "sigmoid", 100),
     4: Config(4, "amazon-deep", 1_600_000, 4.5, 2.1, 2.5e5, 16_000, 1000, [200, 1024, 1024, 1024, 1024, 1024], "bf16", "none"),
     5: Config(5, "amazon-dp", 1_600_000, 80.0, 2.1, 0.0, 20_000, 3000, [200, 1024, 1024, 1024], "tf32", "sigmoid", 107, dp=True),
