@@ -240,13 +240,15 @@ def run_reference(args, cfg):
     return 0
 
 
-def run_gpu_sampled(args, cfg, ctx, runner, stream, dev, rank):
-    """Training loop fed by the GPU frontier sampler (NEXT #3, Alg. 2 on the device): the parent
-    graph and a seeded parent feature matrix (and labels) live in HBM; every --sampler-pool steps
-    one gsg_frontier_sample call draws that many subgraphs; each step copies its CSR into the
-    step's subgraph (device to device), gathers X_s = X[V_s] and the labels (gsg_gather_rows,
-    Alg. 1 line 5), normalizes and runs the layers eagerly (subgraph sizes vary, so no graph).
-    Returns the loop's edge-features/s including the sampling, and the sampler's share."""
+def run_gpu_sampled(args, cfg, ctx, runner, stream, dev, rank, nnz_hint):
+    """Training loop fed by the GPU frontier sampler (NEXT #3, Alg. 2 on the device; Alg. 7's pool
+    refill, P:963-975): the parent graph, a seeded parent feature matrix and labels live in HBM;
+    one gsg_frontier_sample call draws --sampler-pool subgraphs; ONE CUDA graph of the step --
+    gsg_sample_load of sample *d_k into a device-sized subgraph (sizes read on the device,
+    *d_k advanced by the graph itself), X_s = X[V_s] and label gathers (Alg. 1 line 5),
+    normalize, layers, head (per-node loss weights 1/n_k), backward -- is captured per sampled
+    batch and replayed once per sample. The timed region covers the sampling calls, the graph
+    captures and every replay. Returns edge-features/s of the loop and the sampler's share."""
     import torch
     import paper_2010_03166_b200 as gsg
     P = max(1, args.sampler_pool)
@@ -255,6 +257,7 @@ def run_gpu_sampled(args, cfg, ctx, runner, stream, dev, rank):
     gen = torch.Generator(device=dev)
     gen.manual_seed(cfg.seed(2, 0, rank) + 7)
     f0 = cfg.dims[0]
+    n_pad = runner.n_max
     with torch.cuda.stream(stream):
         Xpar = torch.randn((pc.n, wl.ld_for(f0)), device=dev, generator=gen)[:, :f0]
         if cfg.head == "softmax":
@@ -263,60 +266,82 @@ def run_gpu_sampled(args, cfg, ctx, runner, stream, dev, rank):
             Lpar = (torch.rand((pc.n, cfg.classes), device=dev, generator=gen) < cfg.label_p).to(torch.uint8)
         else:
             Lpar = None
-        n_max = runner.n_max
-        Xs = torch.zeros((n_max, wl.ld_for(f0)), device=dev)[:, :f0]
-        Ls = None if Lpar is None else torch.zeros((n_max, Lpar.shape[1]), dtype=Lpar.dtype, device=dev)
+        Xs = torch.zeros((n_pad, wl.ld_for(f0)), device=dev)[:, :f0]
+        Ls = None if Lpar is None else torch.zeros((n_pad, Lpar.shape[1]), dtype=Lpar.dtype, device=dev)
         dH = None
         if cfg.head == "none":
-            dH = torch.randn((n_max, wl.ld_for(cfg.dims[-1])), device=dev, generator=gen)[:, :cfg.dims[-1]]
-    g0 = wl.sample_subgraph(cfg, 0, rank)
-    sgl = ctx.upload(g0.indptr, g0.indices, validate=False)
-    state = {"batch": None, "sample_ms": 0.0}
+            dH = torch.randn((n_pad, wl.ld_for(cfg.dims[-1])), device=dev, generator=gen)[:, :cfg.dims[-1]]
+        d_k = torch.zeros(1, dtype=torch.int32, device=dev)
+        nodes = torch.zeros(n_pad, dtype=torch.int32, device=dev)
+        node_w = torch.zeros(n_pad, dtype=torch.float32, device=dev)
+    sgd = ctx.create_device(n_pad, int(2 * nnz_hint))
     seed0 = cfg.seed(10, 0, rank) + 777
+    labels = None if Ls is None else (Ls[:, 0] if cfg.head == "softmax" else Ls)
 
-    def gs_step(i):
-        if i % P == 0:
-            if state["batch"] is not None:
-                stream.synchronize()
-                state["batch"].free()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            state["batch"] = pg.sample(cfg.n, cfg.m, seed0 + i, count=P)
-            b.record(stream)
-            state["events"] = (a, b)
-        info = state["batch"].get(i % P)
-        n, nnz = info["n"], info["nnz"]
+    def one(batch):
+        batch.load(ctx, d_k, sgd, nodes, node_w)
+        ctx.gather_rows(Xpar, nodes.data_ptr(), Xs, n_pad)
+        if Ls is not None:
+            ctx.gather_rows(Lpar, nodes.data_ptr(), Ls, n_pad)
+        runner.forward_backward(sgd, Xs, labels=labels, dH_top=dH, node_w=node_w if cfg.head != "none" else None)
+
+    def run_batch(b, timed):
+        """Sample one batch, capture the step, replay it P times; returns (work, sampler ms)."""
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        batch = pg.sample(cfg.n, cfg.m, seed0 + b * P, count=P)
+        e.record(stream)
+        work = 0
+        for k in range(P):
+            info = batch.get(k)
+            work += runner.work_edge_features(info["nnz"] + info["n"])
         with torch.cuda.stream(stream):
-            sgl.assign(n, nnz, info["d_indptr"], info["d_indices"])
-            ctx.gather_rows(Xpar, info["d_nodes"], Xs, n)
-            if Ls is not None:
-                ctx.gather_rows(Lpar, info["d_nodes"], Ls, n)
-            labels = None if Ls is None else (Ls[:n, 0] if cfg.head == "softmax" else Ls[:n])
-            runner.forward_backward(sgl, Xs[:n], labels=labels, dH_top=None if dH is None else dH[:n])
-        return runner.work_edge_features(nnz + n)
+            d_k.zero_()
+            if not timed:
+                one(batch)  # eager warm-up: workspaces grow outside any capture
+                d_k.zero_()
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            one(batch)
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            r0.record(stream)
+            for _ in range(P):
+                g.replay()
+            r1.record(stream)
+        stream.synchronize()
+        batch.check()
+        samp = a.elapsed_time(e)
+        replay_ms[0] += r0.elapsed_time(r1)
+        del g
+        batch.free()
+        return work, samp
 
-    for i in range(P):  # warm-up: one full pool
-        gs_step(i)
-    stream.synchronize()
-    steps = 2 * P
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    replay_ms = [0.0]
+    run_batch(0, False)  # warm-up batch
+    replay_ms[0] = 0.0
+    nb = max(1, args.sampler_batches)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(stream)
     work, samp_ms = 0, 0.0
-    e0.record(stream)
-    for i in range(P, P + steps):
-        work += gs_step(i)
-        if i % P == 0:
-            stream.synchronize()
-            samp_ms += state["events"][0].elapsed_time(state["events"][1])
-    e1.record(stream)
+    for b in range(1, nb + 1):
+        w, sm = run_batch(b, True)
+        work += w
+        samp_ms += sm
+    t1.record(stream)
     stream.synchronize()
-    ms = e0.elapsed_time(e1)
-    state["batch"].free()
+    ms = t0.elapsed_time(t1)
+    steps = nb * P
+    sgd.free()
     pg.free()
     return {"value": work / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
             "subgraphs_per_gpu_sampler_call": P, "sampler_ms_per_subgraph": samp_ms / steps,
-            "sampler_share": samp_ms / ms,
-            "note": "fresh GPU-sampled subgraph every step (eager launches), features / labels gathered from "
-                    "parent arrays in HBM; includes the sampling kernels"}
+            "sampler_share": samp_ms / ms, "launch_mode": "one CUDA graph per sampled batch (gsg_sample_load)",
+            "replay_ms_per_step": replay_ms[0] / steps,
+            "note": "fresh GPU-sampled subgraph every step; the timed region includes the sampling calls "
+                    "(gsg_frontier_sample, host-synchronized), the graph capture per batch and every replay"}
 
 
 # ------------------------------------------------------------------------------ our arm
@@ -346,8 +371,10 @@ def main():
                     help="gpu: additionally time a training loop whose subgraphs are frontier-sampled on the GPU "
                          "(NEXT #3) from a device-resident parent graph, features gathered from a parent feature "
                          "matrix in HBM, a fresh subgraph every step")
-    ap.add_argument("--sampler-pool", type=int, default=296,
-                    help="subgraphs per GPU sampling call (--sampler gpu; 2 per SM keeps the latency-bound sampler busy)")
+    ap.add_argument("--sampler-pool", type=int, default=888,
+                    help="subgraphs per GPU sampling call (--sampler gpu; 6 per SM keep the latency-bound samplers busy)")
+    ap.add_argument("--sampler-batches", type=int, default=2,
+                    help="timed sampling calls of --sampler gpu (each followed by --sampler-pool graph replays)")
     ap.add_argument("--nccl-timeout-ms", type=int, default=300000,
                     help="gsg_nccl_wait time-out for the all-reduce (a stalled or dead peer aborts the run)")
     ap.add_argument("--flush-l2", action="store_true",
@@ -848,7 +875,7 @@ def main():
     # ---- optional: the same step fed by the GPU sampler (a fresh subgraph every step) ----
     gpu_loop = None
     if args.sampler == "gpu" and args.batch == 1:
-        gpu_loop = run_gpu_sampled(args, cfg, ctx, runner, stream, dev, rank)
+        gpu_loop = run_gpu_sampled(args, cfg, ctx, runner, stream, dev, rank, max(nnz_raw))
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -366,10 +366,31 @@ GSG_API int gsg_sample_get(gsg_sample_t s, int32_t k, int32_t* n_k, int64_t* nnz
                            const int64_t** d_indptr, const int32_t** d_indices,
                            const int32_t** d_nodes);
 GSG_API int gsg_sample_free(gsg_sample_t s);
+/* A subgraph whose sizes live on the device, so that one captured CUDA graph of the training
+ * step serves every GPU-sampled subgraph (Alg. 7's pool refill, with Alg. 2 on the
+ * device): n (>= 1) nodes fixed at creation, up to nnz_cap raw entries; the actual entry count is
+ * indptr[n] on the device. Filled by gsg_sample_load; normalize / SpMM / layer calls then take
+ * every size from device memory (host-side sizes are the capacities). Starts as an empty graph.
+ * Errors: GSG_EINVAL (n < 1, nnz_cap < 0, NULL out), GSG_ENOMEM. Free with gsg_subgraph_free. */
+GSG_API int gsg_subgraph_create_device(gsg_ctx_t ctx, int32_t n, int64_t nnz_cap, gsg_subgraph_t* out);
+/* Loads sample *d_k of a gsg_frontier_sample batch into the device-sized subgraph sg, stream
+ * ordered and CUDA-graph capturable, then advances *d_k = (*d_k + 1) mod count (d_k: one int32
+ * in DEVICE memory, 0 <= *d_k < count). Sample k (n_k nodes, nnz_k entries) occupies nodes
+ * 0..n_k-1 of sg; nodes n_k..n-1 are isolated padding (empty rows: normalization gives them
+ * their self loop only). Optional outputs (device, n entries): d_nodes_out[i] = the parent id of
+ * node i, or -1 for padding (gsg_gather_rows writes zero rows for -1: X_s = X[V_s], Alg. 1
+ * line 5); d_node_w[i] = 1/n_k for real nodes and 0 for padding -- as gsg_head's node_w the loss
+ * and dS equal those of the n_k-node subgraph (a zero feature row stays zero through the layers,
+ * so padding adds nothing to any dW). A sample with n_k > n or nnz_k > nnz_cap leaves sg empty
+ * and sets an error flag read by gsg_sample_check. Errors: GSG_EINVAL (NULL, sg not device-sized). */
+GSG_API int gsg_sample_load(gsg_ctx_t ctx, gsg_sample_t s, int32_t* d_k, gsg_subgraph_t sg,
+                            int32_t* d_nodes_out, float* d_node_w);
+/* GSG_OK, or GSG_EINVAL if some gsg_sample_load of this batch did not fit (synchronous). */
+GSG_API int gsg_sample_check(gsg_sample_t s);
 /* Row gather for the sampled subgraph's inputs (Alg. 1 line 5: X_s = X[V_s], the labels
  * likewise): dst row r (row_bytes bytes, pitch dst_pitch) = src row d_idx[r] (pitch src_pitch),
  * r < rows, all DEVICE pointers (e.g. d_nodes of gsg_sample_get into a parent feature matrix
- * resident in HBM). 16-byte vectors when all pointers, pitches and row_bytes are 16-byte
+ * resident in HBM); d_idx[r] < 0 writes a zero row (padding nodes of gsg_sample_load). 16-byte vectors when all pointers, pitches and row_bytes are 16-byte
  * multiples. Errors: GSG_EINVAL (negative sizes, NULL, pitch < row_bytes). */
 GSG_API int gsg_gather_rows(gsg_ctx_t ctx, int32_t rows, int64_t row_bytes, const void* d_src,
                             int64_t src_pitch, const int32_t* d_idx, void* d_dst, int64_t dst_pitch);

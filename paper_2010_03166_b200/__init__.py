@@ -84,6 +84,9 @@ _SIGS = {
     "gsg_nccl_comm_destroy": (_int, [_vp]),
     "gsg_allreduce_grads": (_int, [_vp, _vp, _vp, _vp, _int, _int]),
     "gsg_nccl_wait": (_int, [_vp, _vp, _i64]),
+    "gsg_subgraph_create_device": (_int, [_vp, _i32, _i64, ctypes.POINTER(_vp)]),
+    "gsg_sample_load": (_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "gsg_sample_check": (_int, [_vp]),
     "gsg_diag_gather_ceiling": (_int, [_vp, _vp, _i32, _i64, _i32, ctypes.POINTER(ctypes.c_double)]),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -231,6 +234,14 @@ class SampleBatch:
         """Copy sample k back (tests): (indptr int64, indices int32, nodes int32) numpy arrays."""
         return tuple(t.cpu().numpy() for t in self.tensors(k))
 
+    def load(self, ctx: "Context", d_k, sg: "Subgraph", nodes_out=None, node_w=None):
+        """gsg_sample_load: sample d_k[0] (device int32 tensor) into the device-sized subgraph sg,
+        then d_k[0] = (d_k[0] + 1) % count. Graph-capturable."""
+        check(gsg_sample_load(ctx.h, self.h, _ptr(d_k), sg.h, _ptr(nodes_out) or None, _ptr(node_w) or None))
+
+    def check(self):
+        check(gsg_sample_check(self.h))
+
     def free(self):
         if self.h:
             gsg_sample_free(self.h)
@@ -323,6 +334,12 @@ class Context:
         check(gsg_subgraph_upload_device(self.h, n, nnz, _ptr(d_indptr), _ptr(d_indices) or None,
                                          _ptr(d_values) or None, ctypes.byref(out)))
         return Subgraph(self, out.value, n, nnz)
+
+    def create_device(self, n: int, nnz_cap: int) -> Subgraph:
+        """gsg_subgraph_create_device: n nodes, room for nnz_cap raw entries; sizes on the device."""
+        out = _vp()
+        check(gsg_subgraph_create_device(self.h, n, nnz_cap, ctypes.byref(out)))
+        return Subgraph(self, out.value, n, nnz_cap)
 
     # ---- kernels ----
     def gather_rows(self, src, idx_ptr: int, dst, rows: int):

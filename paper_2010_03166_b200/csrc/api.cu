@@ -380,6 +380,7 @@ GSG_API int gsg_subgraph_assign(gsg_ctx_t c, gsg_subgraph_t sg, int32_t n, int64
   sg->n = n;
   sg->nnz = nnz;
   sg->norm_mode = -1;
+  sg->dev_sized = false;
   sg->has_values = h_values != nullptr;
   // cudaMemcpyDefault: host (pinned or pageable) or device source arrays (UVA)
   GSG_CUDA(cudaMemcpyAsync(sg->indptr, h_indptr, sizeof(int64_t) * (n + 1), cudaMemcpyDefault, c->stream));
@@ -415,6 +416,20 @@ GSG_API int gsg_subgraph_upload_device(gsg_ctx_t c, int32_t n, int64_t nnz, cons
   return GSG_OK;
 }
 
+GSG_API int gsg_subgraph_create_device(gsg_ctx_t c, int32_t n, int64_t nnz_cap, gsg_subgraph_t* out) {
+  if (int rc = check_ctx(c)) return rc;
+  GSG_CHECK(out, GSG_EINVAL, "out is NULL");
+  *out = nullptr;
+  GSG_CHECK(n >= 1 && nnz_cap >= 0, GSG_EINVAL, "bad device-sized subgraph n=%d nnz_cap=%lld", n, (long long)nnz_cap);
+  DeviceGuard dg(c->device);
+  gsg_subgraph* sg = nullptr;
+  if (int rc = alloc_subgraph(c, n, nnz_cap, false, &sg)) return rc;
+  sg->dev_sized = true;
+  GSG_CUDA(cudaMemsetAsync(sg->indptr, 0, sizeof(int64_t) * (n + 1), c->stream));  // an empty graph until loaded
+  *out = sg;
+  return GSG_OK;
+}
+
 GSG_API int gsg_subgraph_normalize(gsg_ctx_t c, gsg_subgraph_t sg, int mode) {
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
@@ -431,8 +446,11 @@ GSG_API int gsg_subgraph_info(gsg_ctx_t c, gsg_subgraph_t sg, int32_t* n, int64_
   GSG_CUDA(cudaStreamSynchronize(c->stream));
   int32_t cnt[2] = {0, 0};
   if (sg->norm_mode >= 0) GSG_CUDA(cudaMemcpy(cnt, sg->counters + kBins, sizeof(cnt), cudaMemcpyDeviceToHost));
+  int32_t nh_dev = 0;  // device-sized subgraph: the entry count of Â is rowptr[n]
+  if (sg->dev_sized && sg->norm_mode >= 0)
+    GSG_CUDA(cudaMemcpy(&nh_dev, sg->rowptr + sg->n, sizeof(int32_t), cudaMemcpyDeviceToHost));
   if (n) *n = sg->n;
-  if (nnz_hat) *nnz_hat = sg->norm_mode >= 0 ? sg->nnz_hat : -1;
+  if (nnz_hat) *nnz_hat = sg->norm_mode >= 0 ? (sg->dev_sized ? (int64_t)nh_dev : sg->nnz_hat) : -1;
   if (max_deg) *max_deg = sg->norm_mode >= 0 ? cnt[1] : -1;
   if (n_heavy) *n_heavy = sg->norm_mode >= 0 ? cnt[0] : -1;
   return GSG_OK;
@@ -444,7 +462,12 @@ GSG_API int gsg_subgraph_download(gsg_ctx_t c, gsg_subgraph_t sg, int64_t* h_ind
   GSG_CHECK(sg && sg->norm_mode >= 0, GSG_EINVAL, "subgraph missing or not normalized");
   DeviceGuard dg(c->device);
   GSG_CUDA(cudaStreamSynchronize(c->stream));
-  const int64_t nh = sg->nnz_hat;
+  int64_t nh = sg->nnz_hat;
+  if (sg->dev_sized) {
+    int32_t v = 0;
+    GSG_CUDA(cudaMemcpy(&v, sg->rowptr + sg->n, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    nh = v;
+  }
   if (h_indptr) {
     std::vector<int32_t> tmp(sg->n + 1);
     GSG_CUDA(cudaMemcpy(tmp.data(), sg->rowptr, sizeof(int32_t) * (sg->n + 1), cudaMemcpyDeviceToHost));

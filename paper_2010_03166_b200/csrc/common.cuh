@@ -117,6 +117,8 @@ struct gsg_subgraph {
   int32_t cap_n = 0;        // allocated capacity (gsg_subgraph_assign reuses arrays)
   int64_t cap_nnz = 0;
   bool has_values = false;
+  bool dev_sized = false;   // gsg_subgraph_create_device: n is fixed, the entry count lives on the
+                            // device (indptr[n]); host nnz / nnz_hat are capacities
   // raw structure (device)
   int64_t* indptr = nullptr;    // [n+1]
   int32_t* indices = nullptr;   // [nnz]

@@ -169,9 +169,16 @@ __global__ void k_gather_rows(int rows, int64_t row_bytes, const uint8_t* __rest
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
-    const uint8_t* s = src + (int64_t)__ldg(idx + r) * sp;
+    const int32_t j = __ldg(idx + r);
+    const uint8_t* s = src + (int64_t)j * sp;
     uint8_t* d = dst + (int64_t)r * dp;
-    if (vec) {
+    if (j < 0) {  // a padding row (gsg_sample_load): zeros
+      if (vec) {
+        for (int64_t k = lane; k < row_bytes / 16; k += 32) reinterpret_cast<uint4*>(d)[k] = make_uint4(0, 0, 0, 0);
+      } else {
+        for (int64_t k = lane; k < row_bytes; k += 32) d[k] = 0;
+      }
+    } else if (vec) {
       for (int64_t k = lane; k < row_bytes / 16; k += 32)
         reinterpret_cast<uint4*>(d)[k] = __ldg(reinterpret_cast<const uint4*>(s) + k);
     } else {

@@ -73,10 +73,11 @@ __global__ void k_rows(int n, const int64_t* __restrict__ indptr, const int32_t*
 // (Âᵀ_ij = Â_ji: 1/(d_j+1) row-self, 1/d_j row, val itself for the symmetric mode), written
 // here in the same fp64 -> fp32 rounding as Â_ji, so valT is bit-for-bit the permutation of
 // val that Alg. 4 produces. GSG_NORM_VALUES needs the search (k_transpose_vals).
-__global__ void k_fill(int64_t nnz, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
-                       const float* __restrict__ values, int mode, const int32_t* __restrict__ rowid,
-                       const float* __restrict__ rowval, int32_t* __restrict__ col, float* __restrict__ val,
-                       float* __restrict__ valT) {
+__global__ void k_fill(int64_t nnz, const int64_t* __restrict__ nnz_dev, const int64_t* __restrict__ indptr,
+                       const int32_t* __restrict__ indices, const float* __restrict__ values, int mode,
+                       const int32_t* __restrict__ rowid, const float* __restrict__ rowval, int32_t* __restrict__ col,
+                       float* __restrict__ val, float* __restrict__ valT) {
+  if (nnz_dev) nnz = *nnz_dev;  // device-sized subgraph: the entry count is indptr[n]
   const int self = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_SYM_SELF);
   const bool by_row = (mode == GSG_NORM_ROW_SELF || mode == GSG_NORM_ROW);
   const int64_t T = (int64_t)gridDim.x * blockDim.x;
@@ -201,8 +202,9 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
     if (sg->nnz > 0) {
       int64_t eg = (sg->nnz + T - 1) / T;
       if (eg > (int64_t)ctx->num_sms * 16) eg = (int64_t)ctx->num_sms * 16;
-      k_fill<<<(int)eg, T, 0, st>>>(sg->nnz, sg->indptr, sg->indices, sg->has_values ? sg->values : nullptr, mode,
-                                    sg->rowid, sg->rowval, sg->col, sg->val, sg->valT);
+      k_fill<<<(int)eg, T, 0, st>>>(sg->nnz, sg->dev_sized ? sg->indptr + n : nullptr, sg->indptr, sg->indices,
+                                    sg->has_values ? sg->values : nullptr, mode, sg->rowid, sg->rowval, sg->col,
+                                    sg->val, sg->valT);
       count_launch(ctx);
     }
     if (mode == GSG_NORM_VALUES) {

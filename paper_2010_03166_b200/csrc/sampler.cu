@@ -10,6 +10,7 @@
 // ascending local ids are prefix popcounts, and each (sample, node) warp compacts the parent
 // neighbor list with ballots -- rows come out ascending because the parent rows are ascending
 // and the rank map is monotone (the precondition of Alg. 4).
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -22,6 +23,7 @@ struct gsg_parent {
   int32_t* indices = nullptr;
   int32_t* noniso = nullptr;  // ascending non-isolated node ids
   int64_t n_noniso = 0;
+  int64_t max_deg = 0;
 };
 
 struct gsg_sample {
@@ -32,6 +34,9 @@ struct gsg_sample {
   int32_t* nodes = nullptr;    // [count][n_cap]
   int64_t* indptr = nullptr;   // [count][n_cap + 1]
   int32_t* indices = nullptr;  // concatenated
+  int32_t* d_n = nullptr;      // [count] n_k on the device (gsg_sample_load)
+  int64_t* d_idx_off = nullptr;  // [count] offset of sample k in indices
+  int32_t* d_err = nullptr;    // gsg_sample_load: a sample did not fit the subgraph (checked by gsg_sample_check)
 };
 
 namespace gsg {
@@ -48,36 +53,72 @@ __device__ __forceinline__ uint32_t below(uint64_t r, uint32_t N) { return (uint
 
 __device__ __forceinline__ bool bit_get(const uint32_t* b, int64_t v) { return (b[v >> 5] >> (v & 31)) & 1u; }
 
-// One warp per sampler; lane 0 runs Alg. 2. Shared: FS node ids, degrees, row starts, Fenwick.
+// 32-bit shared-window accesses for the frontier state (the descent below is a chain of
+// dependent shared loads: generic addressing re-derived the window every step).
+template <typename T> __device__ __forceinline__ T lds(uint32_t a);
+template <> __device__ __forceinline__ int32_t lds<int32_t>(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+template <> __device__ __forceinline__ int64_t lds<int64_t>(uint32_t a) {
+  int64_t v;
+  asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, int32_t v) { asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ void sts(uint32_t a, int64_t v) { asm volatile("st.shared.s64 [%0], %1;" ::"r"(a), "l"(v) : "memory"); }
+
+// One warp per sampler; lane 0 runs Alg. 2. Shared memory holds the frontier's degrees, row
+// starts and a Fenwick tree over the degrees (FenT / StartT: int32 whenever the frontier degree
+// sum / the parent's entry count fit: 36 KB at m = 3000, so ~6 samplers share an SM instead of
+// 2). The V_s membership test of iteration i's new node (a bitmap word in global memory) is
+// issued at the end of iteration i and consumed only after iteration i+1's neighbor pick has
+// been issued, so the two global accesses overlap; if consuming it completes V_s, iteration
+// i+1 is abandoned before it changes any state -- the sampled set is exactly the serial Alg. 2's.
+template <typename FenT, typename StartT>
 __global__ void k_frontier(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                            const int32_t* __restrict__ noniso, int64_t n_noniso, int n, int m, int clip,
                            uint64_t seed, int64_t words, uint32_t* __restrict__ bitmaps, int32_t* __restrict__ vs_all,
                            int32_t* __restrict__ nv_out) {
   extern __shared__ int64_t sm64[];
-  int64_t* fen = sm64;                                             // [m + 1]
-  int64_t* fstart = fen + (m + 1);                                 // [m]
-  int32_t* fnode = reinterpret_cast<int32_t*>(fstart + m);         // [m]
-  int32_t* fdeg = fnode + m;                                       // [m]
+  FenT* fen = reinterpret_cast<FenT*>(sm64);                                    // [m + 1]
+  StartT* fstart = reinterpret_cast<StartT*>(fen + (m + 1 + 1) / 2 * 2);        // [m] (8-byte aligned)
+  int32_t* fdeg = reinterpret_cast<int32_t*>(fstart + (m + 1) / 2 * 2);         // [m]
+  const uint32_t fen_s = (uint32_t)__cvta_generic_to_shared(fen);
+  const uint32_t fstart_s = (uint32_t)__cvta_generic_to_shared(fstart);
+  const uint32_t fdeg_s = (uint32_t)__cvta_generic_to_shared(fdeg);
   const int s = blockIdx.x;
-  if (threadIdx.x != 0) return;
+  const int lane = threadIdx.x;
   const uint64_t sd = mix64(mix64(seed) + (uint64_t)s);  // gsg.h: seed_k (decorrelated across calls)
   uint32_t* bits = bitmaps + (int64_t)s * words;
   int32_t* vs = vs_all + (int64_t)s * n;
-  // FS_0: m distinct nodes, uniform over the non-isolated nodes (attempt counter t)
+  // FS_0: m distinct nodes, uniform over the non-isolated nodes (attempt counter t). The
+  // candidates c_t do not depend on the state, so the warp draws 32 attempts at once; attempt t
+  // is accepted iff c_t is not in V_s yet and no earlier attempt of the batch drew it, and only
+  // the first m - cnt acceptances count -- exactly the serial rejection loop.
   int cnt = 0;
-  for (uint64_t t = 0; cnt < m; t++) {
-    const int32_t c = noniso[below(rng(sd, t, 3), (uint32_t)n_noniso)];
-    if (bit_get(bits, c)) continue;
-    bits[c >> 5] |= 1u << (c & 31);
-    const int64_t b0 = indptr[c];
-    fnode[cnt] = c;
-    fstart[cnt] = b0;
-    fdeg[cnt] = (int32_t)(indptr[c + 1] - b0);
-    vs[cnt] = c;
-    cnt++;
+  for (uint64_t t0 = 0; cnt < m; t0 += 32) {
+    const int32_t c = noniso[below(rng(sd, t0 + lane, 3), (uint32_t)n_noniso)];
+    const unsigned same = __match_any_sync(0xffffffffu, c);
+    const bool fresh = !bit_get(bits, c) && !(same & ((1u << lane) - 1u));
+    const unsigned acc = __ballot_sync(0xffffffffu, fresh);
+    const int rank = __popc(acc & ((1u << lane) - 1u));
+    const int need = m - cnt;
+    if (fresh && rank < need) {
+      atomicOr(&bits[c >> 5], 1u << (c & 31));
+      const int64_t b0 = indptr[c];
+      fstart[cnt + rank] = (StartT)b0;
+      fdeg[cnt + rank] = (int32_t)(indptr[c + 1] - b0);
+      vs[cnt + rank] = c;
+    }
+    cnt += min(__popc(acc), need);
+    __syncwarp();
   }
+  __threadfence_block();
+  if (lane != 0) return;
   // Fenwick tree over the frontier degrees (1-based)
-  int64_t total = 0;
+  FenT total = 0;
   for (int i = 1; i <= m; i++) { fen[i] = fdeg[i - 1]; total += fdeg[i - 1]; }
   for (int i = 1; i <= m; i++) {
     const int j = i + (i & -i);
@@ -87,31 +128,54 @@ __global__ void k_frontier(const int64_t* __restrict__ indptr, const int32_t* __
   while (top * 2 <= m) top *= 2;
   int nv = m;
   const uint64_t max_it = 1000ull * n + 1000000ull;
-  for (uint64_t it = 0; nv < n && it < max_it; it++) {
+  int32_t pend = -1;   // new frontier node of the previous iteration, membership not yet tested
+  uint32_t pword = 0;  // its bitmap word (load in flight)
+  for (uint64_t it = 0; nv < n; it++) {
+    if (it == max_it) break;
     // Alg. 2 line 4: slot with probability deg(u) / sum_FS deg  (smallest slot with prefix > x)
-    int64_t x = below(rng(sd, it, 0), (uint32_t)total);
+    FenT x = (FenT)below(rng(sd, it, 0), (uint32_t)total);
+    const uint64_t r1 = rng(sd, it, 1);
     int pos = 0;
-    for (int step = top; step > 0; step >>= 1) {
-      if (pos + step <= m && fen[pos + step] <= x) { pos += step; x -= fen[pos]; }
+#pragma unroll
+    for (int lv = 13; lv >= 0; lv--) {  // m <= 16384: top <= 2^13
+      const int step = 1 << lv;
+      if (step <= top && pos + step <= m) {
+        const FenT v = lds<FenT>(fen_s + (uint32_t)(pos + step) * sizeof(FenT));
+        if (v <= x) { pos += step; x -= v; }
+      }
     }
     const int slot = pos;
-    const int32_t du = fdeg[slot];
+    const int32_t du = lds<int32_t>(fdeg_s + 4u * slot);
     // line 5: uniform neighbor u' of u
-    const int32_t up = indices[fstart[slot] + below(rng(sd, it, 1), (uint32_t)du)];
-    const int64_t bu = indptr[up];
-    const int32_t dup = (int32_t)(indptr[up + 1] - bu);
-    // line 6: FS <- FS \ {u} U {u'}
-    fnode[slot] = up;
-    fstart[slot] = bu;
-    fdeg[slot] = dup;
-    const int64_t delta = (int64_t)dup - du;
-    for (int i = slot + 1; i <= m; i += i & -i) fen[i] += delta;
-    total += delta;
-    // R9: the new frontier node joins V_s
-    if (!bit_get(bits, up)) {
-      bits[up >> 5] |= 1u << (up & 31);
-      vs[nv++] = up;
+    const int32_t up = indices[(int64_t)lds<StartT>(fstart_s + (uint32_t)sizeof(StartT) * slot) + below(r1, (uint32_t)du)];
+    const int64_t bu = indptr[up], eu = indptr[up + 1];
+    // R9: the previous iteration's new frontier node joins V_s (tested while u' is in flight)
+    if (pend >= 0) {
+      if (!((pword >> (pend & 31)) & 1u)) {
+        // pword is the word's current value (loaded after every earlier set; only this thread
+        // writes this sampler's bitmap): a plain store, no dependent read-modify-write
+        bits[pend >> 5] = pword | (1u << (pend & 31));
+        vs[nv++] = pend;
+      }
+      pend = -1;
+      if (nv >= n) break;  // V_s complete: this iteration never happened
     }
+    // line 6: FS <- FS \ {u} U {u'}
+    const int32_t dup = (int32_t)(eu - bu);
+    sts(fstart_s + (uint32_t)sizeof(StartT) * slot, (StartT)bu);
+    sts(fdeg_s + 4u * slot, dup);
+    const FenT delta = (FenT)dup - (FenT)du;
+    for (int i = slot + 1; i <= m; i += i & -i) {
+      const uint32_t a = fen_s + (uint32_t)i * sizeof(FenT);
+      sts(a, (FenT)(lds<FenT>(a) + delta));
+    }
+    total += delta;
+    pend = up;
+    pword = bits[up >> 5];
+  }
+  if (pend >= 0 && nv < n && !((pword >> (pend & 31)) & 1u)) {  // the last iteration's test (max_it)
+    bits[pend >> 5] |= 1u << (pend & 31);
+    vs[nv++] = pend;
   }
   // clipping to a multiple of `clip` by uniformly random removals
   const int keep = nv / clip * clip;
@@ -241,6 +305,42 @@ __global__ void k_induce_fill(const int64_t* __restrict__ indptr, const int32_t*
   }
 }
 
+// gsg_sample_load: sample *d_k into a device-sized subgraph of n_pad nodes. Nodes n_k .. n_pad-1
+// are isolated padding (empty rows; normalization gives them a self loop, their feature rows are
+// gathered as zeros and their loss weight is 0), so one CUDA graph of the step serves every
+// sample: every size the kernels need is read from device memory.
+__global__ void k_sample_load(const int32_t* __restrict__ d_k, int n_cap, const int32_t* __restrict__ s_n,
+                              const int64_t* __restrict__ s_indptr, const int64_t* __restrict__ s_off,
+                              const int32_t* __restrict__ s_indices, const int32_t* __restrict__ s_nodes, int n_pad,
+                              int64_t nnz_cap, int64_t* __restrict__ indptr, int32_t* __restrict__ indices,
+                              int32_t* __restrict__ nodes_out, float* __restrict__ node_w, int32_t* __restrict__ err) {
+  const int k = *d_k;
+  const int nk = s_n[k];
+  const int64_t* ip = s_indptr + (int64_t)k * (n_cap + 1);
+  const int64_t nnz = ip[nk];
+  if (nk > n_pad || nnz > nnz_cap) {  // does not fit: leave the subgraph empty and flag it
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(err, 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n_pad; i += (int64_t)gridDim.x * blockDim.x)
+      indptr[i] = 0;
+    return;
+  }
+  const int64_t T = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const float w = nk > 0 ? 1.0f / (float)nk : 0.f;
+  for (int64_t i = t0; i <= n_pad; i += T) {
+    indptr[i] = i <= nk ? ip[i] : nnz;
+    if (i < n_pad) {
+      const bool real = i < nk;
+      if (nodes_out) nodes_out[i] = real ? s_nodes[(int64_t)k * n_cap + i] : -1;
+      if (node_w) node_w[i] = real ? w : 0.f;
+    }
+  }
+  const int32_t* src = s_indices + s_off[k];
+  for (int64_t e = t0; e < nnz; e += T) indices[e] = src[e];
+}
+
+__global__ void k_advance(int32_t* d_k, int count) { *d_k = (*d_k + 1) % count; }
+
 }  // namespace
 }  // namespace gsg
 
@@ -264,6 +364,7 @@ GSG_API int gsg_parent_upload(gsg_ctx_t c, int64_t N, int64_t nnz, const int64_t
   p->N = N;
   p->nnz = nnz;
   p->n_noniso = (int64_t)non.size();
+  for (int64_t i = 0; i < N; i++) p->max_deg = std::max<int64_t>(p->max_deg, h_indptr[i + 1] - h_indptr[i]);
   cudaError_t e = cudaMalloc(&p->indptr, sizeof(int64_t) * (N + 1));
   if (e == cudaSuccess) e = cudaMalloc(&p->indices, sizeof(int32_t) * (nnz > 0 ? nnz : 1));
   if (e == cudaSuccess) e = cudaMalloc(&p->noniso, sizeof(int32_t) * (non.size() > 0 ? non.size() : 1));
@@ -320,11 +421,23 @@ GSG_API int gsg_frontier_sample(gsg_ctx_t c, gsg_parent_t p, int32_t n, int32_t 
   e = cudaMemsetAsync(bitmaps.ptr, 0, sizeof(uint32_t) * words * count, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(S->indptr, 0, sizeof(int64_t) * (int64_t)(n + 1) * count, st);
   if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMemsetAsync(sample)"));
-  const size_t smem = sizeof(int64_t) * (2 * (size_t)m + 1) + sizeof(int32_t) * 2 * (size_t)m;
-  e = cudaFuncSetAttribute(k_frontier, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaFuncSetAttribute(k_frontier)"));
-  k_frontier<<<count, 32, smem, st>>>(p->indptr, p->indices, p->noniso, p->n_noniso, n, m, clip, seed, words,
-                                      (uint32_t*)bitmaps.ptr, (int32_t*)vs.ptr, (int32_t*)nv.ptr);
+  // frontier state: 4-byte Fenwick sums / row starts whenever they fit (36 KB for m = 3000:
+  // ~6 samplers per SM), else 8-byte ones
+  const bool fen32 = (int64_t)m * p->max_deg < (int64_t)INT32_MAX, start32 = p->nnz < (int64_t)INT32_MAX;
+  const size_t mm = (size_t)(m + 1) / 2 * 2 + 2;
+  const size_t smem = mm * (fen32 ? 4 : 8) + mm * (start32 ? 4 : 8) + 4 * (size_t)m + 16;
+  auto launch = [&](auto kern) {
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (r != cudaSuccess) return r;
+    kern<<<count, 32, smem, st>>>(p->indptr, p->indices, p->noniso, p->n_noniso, n, m, clip,
+                                  seed, words, (uint32_t*)bitmaps.ptr, (int32_t*)vs.ptr, (int32_t*)nv.ptr);
+    return cudaGetLastError();
+  };
+  if (fen32 && start32) e = launch(k_frontier<int32_t, int32_t>);
+  else if (start32) e = launch(k_frontier<int64_t, int32_t>);
+  else if (fen32) e = launch(k_frontier<int32_t, int64_t>);
+  else e = launch(k_frontier<int64_t, int64_t>);
+  if (e != cudaSuccess) return cleanup(cuda_fail(e, "k_frontier"));
   k_rank<<<count, 1024, 0, st>>>((const uint32_t*)bitmaps.ptr, words, n, (int32_t*)wordpre.ptr, S->nodes);
   const int64_t warps = (int64_t)count * n;
   int grid = (int)std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)c->num_sms * 16);
@@ -350,17 +463,19 @@ GSG_API int gsg_frontier_sample(gsg_ctx_t c, gsg_parent_t p, int32_t n, int32_t 
     S->idx_off[k] = tot;
     tot += v;
   }
-  DevBuf offs;
-  if ((rc = offs.reserve(sizeof(int64_t) * count))) return cleanup(rc);
   e = cudaMalloc(&S->indices, sizeof(int32_t) * (tot > 0 ? tot : 1));
-  if (e == cudaSuccess) e = cudaMemcpyAsync(offs.ptr, S->idx_off.data(), sizeof(int64_t) * count, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) { offs.release(); return cleanup(cuda_fail(e, "cudaMalloc(sample indices)")); }
+  if (e == cudaSuccess) e = cudaMalloc(&S->d_idx_off, sizeof(int64_t) * count);
+  if (e == cudaSuccess) e = cudaMalloc(&S->d_n, sizeof(int32_t) * count);
+  if (e == cudaSuccess) e = cudaMalloc(&S->d_err, sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemsetAsync(S->d_err, 0, sizeof(int32_t), st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(S->d_idx_off, S->idx_off.data(), sizeof(int64_t) * count, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(S->d_n, nv.ptr, sizeof(int32_t) * count, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(sample indices)"));
   k_induce_fill<<<grid, 256, 0, st>>>(p->indptr, p->indices, (const uint32_t*)bitmaps.ptr, words,
                                       (const int32_t*)wordpre.ptr, S->nodes, (const int32_t*)nv.ptr, count, n,
-                                      S->indptr, (const int64_t*)offs.ptr, S->indices);
+                                      S->indptr, S->d_idx_off, S->indices);
   count_launch(c);
   e = cudaStreamSynchronize(st);
-  offs.release();
   bitmaps.release(); vs.release(); nv.release(); wordpre.release();
   if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) {
     gsg_sample_free(S);
@@ -381,12 +496,42 @@ GSG_API int gsg_sample_get(gsg_sample_t s, int32_t k, int32_t* n_k, int64_t* nnz
   return GSG_OK;
 }
 
+GSG_API int gsg_sample_load(gsg_ctx_t c, gsg_sample_t s, int32_t* d_k, gsg_subgraph_t sg, int32_t* d_nodes_out,
+                            float* d_node_w) {
+  GSG_CHECK(c && s && d_k && sg, GSG_EINVAL, "NULL argument");
+  GSG_CHECK(sg->dev_sized, GSG_EINVAL, "gsg_sample_load needs a subgraph from gsg_subgraph_create_device");
+  DeviceGuard dg(c->device);
+  const int64_t work = std::max<int64_t>((int64_t)sg->n + 1, sg->cap_nnz);
+  const int grid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)c->num_sms * 8);
+  k_sample_load<<<grid, 256, 0, c->stream>>>(d_k, s->n_cap, s->d_n, s->indptr, s->d_idx_off, s->indices, s->nodes,
+                                             sg->n, sg->cap_nnz, sg->indptr, sg->indices, d_nodes_out, d_node_w,
+                                             s->d_err);
+  k_advance<<<1, 1, 0, c->stream>>>(d_k, s->count);
+  count_launch(c, 2);
+  sg->norm_mode = -1;
+  GSG_CUDA(cudaGetLastError());
+  return GSG_OK;
+}
+
+GSG_API int gsg_sample_check(gsg_sample_t s) {
+  GSG_CHECK(s, GSG_EINVAL, "NULL sample");
+  DeviceGuard dg(s->device);
+  int32_t e = 0;
+  GSG_CUDA(cudaMemcpy(&e, s->d_err, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  GSG_CHECK(e == 0, GSG_EINVAL, "gsg_sample_load: a sample exceeded the subgraph's node or entry capacity "
+                                "(the subgraph was left empty for that step)");
+  return GSG_OK;
+}
+
 GSG_API int gsg_sample_free(gsg_sample_t s) {
   if (!s) return GSG_OK;
   DeviceGuard dg(s->device);
   cudaFree(s->nodes);
   cudaFree(s->indptr);
   cudaFree(s->indices);
+  cudaFree(s->d_n);
+  cudaFree(s->d_idx_off);
+  cudaFree(s->d_err);
   delete s;
   return GSG_OK;
 }

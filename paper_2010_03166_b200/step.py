@@ -99,12 +99,14 @@ class GCNStep:
         self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
 
     def forward_backward(self, sg: Subgraph, X, labels=None, dH_top=None, comm=None, normalize: bool = True,
-                         before_grads=None, input_grad: bool = True):
+                         before_grads=None, input_grad: bool = True, node_w=None):
         """One step. `before_grads` (optional) is called right before the first write of a weight
         gradient (the head, else the top layer's backward): bench.py uses it to make the step
         wait for the previous step's all-reduce of the same gradient buffer, so that the
         all-reduce overlaps this step's forward. `input_grad=False` skips layer 1's dX (the
-        gradient w.r.t. the input features, which training does not use)."""
+        gradient w.r.t. the input features, which training does not use). `node_w`
+        (optional, device fp32 [n]) are the head's per-node loss weights (gsg_head), e.g. 1/n_k
+        and 0 for the padding nodes of a gsg_sample_load subgraph."""
         ctx, d, n = self.ctx, self.dims, sg.n
         if normalize:
             sg.normalize(GSG_NORM_ROW_SELF)
@@ -129,7 +131,7 @@ class GCNStep:
             kind = GSG_HEAD_SOFTMAX if self.head == "softmax" else GSG_HEAD_SIGMOID
             ctx.head(h, self.Wm, labels, self.S[:n], self.dS[:n], self.dWm, self.dHL[:n], n, d[-1], self.C, kind,
                      self.loss, dHlp=None if self.dHLlp is None else self.dHLlp[:n], precision=self.prec,
-                     HL_bits=self._hb(self.L - 1, n))
+                     node_w=node_w, HL_bits=self._hb(self.L - 1, n))
             dH, dHlp, flags = self.dHL[:n], (None if self.dHLlp is None else self.dHLlp[:n]), GSG_DH_PREMASKED
         else:
             dH, dHlp, flags = dH_top, None, 0

@@ -26,7 +26,7 @@ def main():
     ctx = gsg.Context(0)
     pg = gsg.ParentGraph(ctx, p.indptr, p.indices)
     pg.sample(cfg.n, cfg.m, 1, count=2).free()  # warm-up
-    for count in (1, 16, 148, 444):
+    for count in (1, 16, 148, 444, 888, 1776):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         b = pg.sample(cfg.n, cfg.m, 1000, count=count)
