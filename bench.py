@@ -211,6 +211,19 @@ class OracleSample:
     def cores():
         return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
+    @staticmethod
+    def cpu_model():
+        """The host CPU the oracle ran on (/proc/cpuinfo), as BASELINE.md's plan asks."""
+        try:
+            with open("/proc/cpuinfo") as f:
+                for ln in f:
+                    if ln.lower().startswith("model name"):
+                        return ln.split(":", 1)[1].strip()
+        except OSError:
+            pass
+        import platform
+        return platform.processor() or None
+
 
 def run_reference(args, cfg):
     rank, world, _ = dist_env()
@@ -234,7 +247,8 @@ def run_reference(args, cfg):
            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"config{cfg.cid}:{cfg.name}", "nodes": g.n, "dims": cfg.dims},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "oracle", "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "oracle", "sample": sample,
+                            "cpu_model": OracleSample.cpu_model()},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -868,7 +882,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         osamp = OracleSample(cfg, pool[0], inputs[0])
         w_, dt_ = osamp.calibrate(args.cpu_seconds)
-        cpu = {"value": w_ / dt_, "unit": UNIT, "cores": osamp.cores(), "kind": "oracle",
+        cpu = {"value": w_ / dt_, "unit": UNIT, "cores": osamp.cores(), "kind": "oracle", "cpu_model": osamp.cpu_model(),
                "sample": f"rows [0,{osamp.rows}) of the first subgraph, all {cfg.L} layers fwd+bwd + head, "
                          f"fp64 plain loops, {dt_:.1f} s"}
 

@@ -431,6 +431,7 @@ GSG_API int gsg_subgraph_create_device(gsg_ctx_t c, int32_t n, int64_t nnz_cap, 
 }
 
 GSG_API int gsg_subgraph_normalize(gsg_ctx_t c, gsg_subgraph_t sg, int mode) {
+  NvtxRange nvtx("gsg a1 normalize");
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   DeviceGuard dg(c->device);
@@ -496,6 +497,7 @@ GSG_API int gsg_subgraph_free(gsg_subgraph_t sg) {
 GSG_API int gsg_spmm(gsg_ctx_t c, gsg_subgraph_t sg, int transpose, int32_t f, const float* X, int64_t ldx, float* Y,
                      int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, const uint32_t* mbits,
                      int64_t ldmb) {
+  NvtxRange nvtx("gsg a2/a7 spmm");
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   DeviceGuard dg(c->device);
@@ -509,6 +511,7 @@ GSG_API int gsg_gemm(gsg_ctx_t c, int32_t M, int32_t N, int32_t K, const void* A
                      int64_t ldb, int transB, float* C, int64_t ldc, void* Clp, int64_t ldclp, int precision, int epilogue,
                      const float* aux, int64_t ldaux, const uint32_t* auxbits, int64_t ldauxb, uint32_t* Cbits,
                      int64_t ldcb, int split_k, int accumulate) {
+  NvtxRange nvtx("gsg a3/a5/a6 gemm");
   if (int rc = check_ctx(c)) return rc;
   DeviceGuard dg(c->device);
   return gemm_launch(c, M, N, K, A, lda, transA ? 1 : 0, B, ldb, transB ? 1 : 0, C, ldc, Clp, ldclp, precision,
@@ -525,6 +528,7 @@ GSG_API int gsg_layer_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
                               const float* W, int64_t ldw, float* P, int64_t ldp, void* Plp, int64_t ldplp, float* H,
                               int64_t ldh, void* Hlp, int64_t ldhlp, uint32_t* Hbits, int64_t ldhbits, int precision,
                               int flags) {
+  NvtxRange nvtx("gsg a2-a3 layer_forward");
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   GSG_CHECK(f_in >= 1 && f_out >= 1, GSG_EINVAL, "f_in=%d f_out=%d must be >= 1", f_in, f_out);
@@ -579,6 +583,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
                                const void* dHlp, int64_t lddhlp, const float* W, int64_t ldw, float* dW, int64_t lddw,
                                float* dX, int64_t lddx, void* dXlp, int64_t lddxlp, const float* Hbelow, int64_t ldhb,
                                const uint32_t* Hbelow_bits, int64_t ldhbb, int precision, int flags) {
+  NvtxRange nvtx("gsg a4-a7 layer_backward");
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   GSG_CHECK(f_in >= 1 && f_out >= 1, GSG_EINVAL, "f_in=%d f_out=%d must be >= 1", f_in, f_out);
@@ -681,6 +686,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
 GSG_API int gsg_sage_forward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int32_t fh, const float* X, int64_t ldx,
                              const float* Ws, int64_t ldws, const float* Wn, int64_t ldwn, float* P, int64_t ldp,
                              float* H, int64_t ldh, int precision, int flags) {
+  NvtxRange nvtx("gsg sage_forward");
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   GSG_CHECK(precision == GSG_PREC_TF32 || precision == GSG_PREC_FP32X3, GSG_EUNSUPPORTED,
@@ -702,6 +708,7 @@ GSG_API int gsg_sage_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
                               const float* Ws, int64_t ldws, const float* Wn, int64_t ldwn, float* dWs, int64_t lddws,
                               float* dWn, int64_t lddwn, float* dX, int64_t lddx, const float* Hbelow, int64_t ldhb,
                               int precision, int flags) {
+  NvtxRange nvtx("gsg sage_backward");
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(sg, GSG_EINVAL, "NULL subgraph");
   GSG_CHECK(precision == GSG_PREC_TF32 || precision == GSG_PREC_FP32X3, GSG_EUNSUPPORTED,
@@ -747,6 +754,7 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
                      const float* Wm, int64_t ldw, const void* labels, float* S, float* dS, int64_t lds, float* dWm,
                      int64_t lddw, float* dHL, int64_t lddh, void* dHlp, int64_t lddhlp, float* loss, int precision,
                      const float* node_w, const uint32_t* HLbits, int64_t ldhlb) {
+  NvtxRange nvtx("gsg a8 head");
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(kind == GSG_HEAD_SOFTMAX || kind == GSG_HEAD_SIGMOID, GSG_EINVAL, "bad head kind %d", kind);
   GSG_CHECK(n >= 1 && f >= 1 && C >= 1, GSG_EINVAL, "bad head sizes n=%d f=%d C=%d", n, f, C);
@@ -812,6 +820,7 @@ GSG_API int gsg_nccl_comm_destroy(void* comm) {
 
 GSG_API int gsg_allreduce_grads(gsg_ctx_t c, void* comm, float* const* bufs, const int64_t* counts, int nbufs,
                                 int average) {
+  NvtxRange nvtx("gsg a9 allreduce_grads");
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(comm && bufs && counts && nbufs >= 0, GSG_EINVAL, "bad allreduce arguments");
   Nccl& N = nccl();
@@ -835,6 +844,7 @@ GSG_API int gsg_allreduce_grads(gsg_ctx_t c, void* comm, float* const* bufs, con
 }
 
 GSG_API int gsg_nccl_wait(gsg_ctx_t c, void* comm, int64_t timeout_ms) {
+  NvtxRange nvtx("gsg a9 nccl_wait");
   if (int rc = check_ctx(c)) return rc;
   GSG_CHECK(comm, GSG_EINVAL, "NULL communicator");
   Nccl& N = nccl();

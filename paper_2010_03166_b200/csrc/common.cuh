@@ -6,6 +6,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "gsg.h"
 
 namespace gsg {
@@ -43,6 +45,13 @@ struct DeviceGuard {
     cudaGetDevice(&cur);
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
   }
+};
+
+// NVTX range around a public entry point (header-only NVTX3: a no-op unless a tool such as
+// Nsight Systems injects itself), named by the SURVEY §8(a) row it implements.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 // Grow-only device buffer.

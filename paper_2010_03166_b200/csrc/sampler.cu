@@ -392,6 +392,7 @@ GSG_API int gsg_parent_free(gsg_parent_t p) {
 
 GSG_API int gsg_frontier_sample(gsg_ctx_t c, gsg_parent_t p, int32_t n, int32_t m, int32_t clip, uint64_t seed,
                                 int32_t count, gsg_sample_t* out) {
+  NvtxRange nvtx("gsg sampler frontier_sample");
   GSG_CHECK(c && p && out, GSG_EINVAL, "NULL argument");
   GSG_CHECK(count >= 1 && m >= 1 && m <= n && m <= 16384 && clip >= 1, GSG_EINVAL,
             "bad sampler sizes n=%d m=%d clip=%d count=%d", n, m, clip, count);
@@ -498,6 +499,7 @@ GSG_API int gsg_sample_get(gsg_sample_t s, int32_t k, int32_t* n_k, int64_t* nnz
 
 GSG_API int gsg_sample_load(gsg_ctx_t c, gsg_sample_t s, int32_t* d_k, gsg_subgraph_t sg, int32_t* d_nodes_out,
                             float* d_node_w) {
+  NvtxRange nvtx("gsg sampler sample_load");
   GSG_CHECK(c && s && d_k && sg, GSG_EINVAL, "NULL argument");
   GSG_CHECK(sg->dev_sized, GSG_EINVAL, "gsg_sample_load needs a subgraph from gsg_subgraph_create_device");
   DeviceGuard dg(c->device);

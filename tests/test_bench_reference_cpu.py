@@ -26,6 +26,7 @@ def test_reference_arm_line_on_cpu():
     assert d["metric"] and d["unit"] and d["higher_is_better"] is True
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    assert cb["cpu_model"]  # the host CPU is named (BASELINE.md plan item 3)
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("config1")
