@@ -26,7 +26,11 @@ KEYS = [
 ]
 
 
+DIAG = ("k_gather_probe",)  # measurement kernels of bench.py's roofline (gsg_diag_gather_ceiling), not the step
+
+
 def launches(path):
+    """Per-kernel share of the device time of the step's kernels (diagnostic probes excluded)."""
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h, data = rows[hi], rows[hi + 1:]
@@ -37,6 +41,8 @@ def launches(path):
         v = float(r[vi].replace(",", ""))
         v = v / 1e3 if r[ui] in ("ns", "nsecond") else (v * 1e3 if r[ui] in ("ms", "msecond") else v)
         name = re.sub(r"\(.*", "", r[ki])
+        if any(d in name for d in DIAG):
+            continue
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += v
