@@ -236,7 +236,7 @@ GSG_API int gsg_ctx_destroy(gsg_ctx_t c) {
   cudaStreamSynchronize(c->stream);
   c->ws_splitk.release(); c->ws_splitk_side.release(); c->ws_T.release(); c->ws_dZ.release();
   c->ws_lp0.release(); c->ws_lp1.release(); c->ws_lp2.release(); c->ws_loss.release();
-  c->ws_mega.release(); c->ws_megactr.release();
+  c->ws_mega.release(); c->ws_megactr.release(); c->ws_hseg.release(); c->ws_hsegctr.release();
   for (int i = 0; i < 2; i++) { c->ws_x3[i].release(); c->ws_x3_side[i].release(); }
   for (auto& r : c->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->prof.free_ev) cudaEventDestroy(e);
@@ -489,6 +489,7 @@ GSG_API int gsg_subgraph_free(gsg_subgraph_t sg) {
   cudaFree(sg->indptr); cudaFree(sg->indices); cudaFree(sg->values);
   cudaFree(sg->rowptr); cudaFree(sg->col); cudaFree(sg->val); cudaFree(sg->valT);
   cudaFree(sg->perm); cudaFree(sg->rowval); cudaFree(sg->counters); cudaFree(sg->rowid);
+  cudaFree(sg->htask); cudaFree(sg->hcount);
   delete sg;
   return GSG_OK;
 }

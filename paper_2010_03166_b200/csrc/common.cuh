@@ -17,6 +17,8 @@ constexpr int kMegaMinDeg = 2048;   // deg' >= this -> the row is split over kMe
 constexpr int kMegaSegs = 8;
 constexpr int kBins = 32;           // log2 degree buckets
 constexpr int kNMega = 3 * kBins + 6;  // counters[]: number of mega rows (the first ones in perm)
+constexpr int kHSeg = 256;          // heavy rows are cut into warp segments of <= kHSeg neighbors
+constexpr int kNHSeg = 3 * kBins + 7;  // counters[]: number of heavy-row segments (normalize)
 
 void set_error(const char* fmt, ...);
 int fail(int code, const char* fmt, ...);
@@ -110,6 +112,8 @@ struct gsg_ctx {
   gsg::DevBuf ws_loss;     // per-block loss partials
   gsg::DevBuf ws_x3[2];    // GSG_PREC_FP32X3 split operand copies (A3, B3), context stream
   gsg::DevBuf ws_x3_side[2];  // the same for the GEMMs that may be forked onto the side stream
+  gsg::DevBuf ws_hseg;     // SpMM heavy-row segment partials
+  gsg::DevBuf ws_hsegctr;  // SpMM heavy-row (row, chunk) arrival counters, zero between launches
   gsg::DevBuf ws_mega;     // SpMM mega-row segment partials
   gsg::DevBuf ws_megactr;  // SpMM mega-row (row, chunk) arrival counters, zero between launches
   cudaStream_t side = nullptr;       // fork/join side stream (layer backward: dW next to T -> dX)
@@ -141,6 +145,9 @@ struct gsg_subgraph {
   int32_t* rowid = nullptr;     // [nnz] row of each raw entry (normalize scratch)
   float* rowval = nullptr;      // [n] per-row value of the degree modes (1/(d+1) or 1/d), fp64-rounded
   int32_t* counters = nullptr;  // [kBins + 8]: bucket counts ..., [kBins]=n_heavy, [kBins+1]=max_deg
+  int4* htask = nullptr;        // [segments] heavy-row warp segments: (row, k_begin, k_end, first segment of the row)
+  int32_t* hcount = nullptr;    // [segments] at a row's first segment: its number of segments
+  size_t cap_hseg = 0;
   size_t cap_hat = 0;
 };
 

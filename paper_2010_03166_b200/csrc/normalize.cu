@@ -164,6 +164,48 @@ __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t
   }
 }
 
+// Heavy rows (the first n_heavy of perm, deg' >= kHeavyMinDeg) cut into ceil(deg' / kHSeg)
+// equal warp segments, listed in perm order: htask[s] = (row, k_begin, k_end, first segment of
+// the row), hcount[first] = the row's segment count; counters[kNHSeg] = the number of segments.
+// One block: an exclusive scan of the per-row counts over n_heavy rows, 1024 at a time.
+__global__ void k_heavy_tasks(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ perm,
+                              int32_t* __restrict__ counters, int4* __restrict__ htask, int32_t* __restrict__ hcount) {
+  __shared__ int scan[1024];
+  __shared__ int base;
+  const int n_heavy = counters[kBins];
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int r0 = 0; r0 < n_heavy; r0 += blockDim.x) {
+    const int i = r0 + threadIdx.x;
+    int row = 0, b = 0, d = 0, cnt = 0;
+    if (i < n_heavy) {
+      row = perm[i];
+      b = rowptr[row];
+      d = rowptr[row + 1] - b;
+      cnt = (d + kHSeg - 1) / kHSeg;
+    }
+    scan[threadIdx.x] = cnt;
+    __syncthreads();
+    for (int off = 1; off < (int)blockDim.x; off <<= 1) {  // inclusive Hillis-Steele scan
+      const int v = threadIdx.x >= (unsigned)off ? scan[threadIdx.x - off] : 0;
+      __syncthreads();
+      scan[threadIdx.x] += v;
+      __syncthreads();
+    }
+    const int first = base + scan[threadIdx.x] - cnt;
+    if (i < n_heavy) {
+      const int len = (d + cnt - 1) / cnt;  // equal segments of <= kHSeg neighbors
+      hcount[first] = cnt;
+      for (int s = 0; s < cnt; s++)
+        htask[first + s] = make_int4(row, b + s * len, min(b + d, b + (s + 1) * len), first);
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) base += scan[threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) counters[kNHSeg] = base;
+}
+
 }  // namespace
 
 int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
@@ -186,6 +228,16 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   }
   sg->nnz_hat = nh;
   sg->norm_mode = mode;
+  {  // heavy-row segments: sum over heavy rows of ceil(deg'/kHSeg) <= nnz'/kHSeg + nnz'/kHeavyMinDeg
+    const size_t cap = (size_t)(nh / kHSeg + nh / kHeavyMinDeg + 1);
+    if (cap > sg->cap_hseg) {
+      cudaFree(sg->htask); cudaFree(sg->hcount);
+      sg->htask = nullptr; sg->hcount = nullptr;
+      GSG_CUDA(cudaMalloc(&sg->htask, sizeof(int4) * cap));
+      GSG_CUDA(cudaMalloc(&sg->hcount, sizeof(int32_t) * cap));
+      sg->cap_hseg = cap;
+    }
+  }
   ProfScope ps(ctx, GSG_K_NORM, 16.0 * nh + 24.0 * n, 0.0);
   GSG_CUDA(cudaMemsetAsync(sg->counters, 0, sizeof(int32_t) * (3 * kBins + 8), st));
   const int T = 256;
@@ -212,7 +264,8 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
       count_launch(ctx);
     }
     k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm);
-    count_launch(ctx);
+    k_heavy_tasks<<<1, 1024, 0, st>>>(sg->rowptr, sg->perm, sg->counters, sg->htask, sg->hcount);
+    count_launch(ctx, 2);
   }
   GSG_CUDA(cudaGetLastError());
   return GSG_OK;

@@ -64,6 +64,13 @@ struct SpmmArgs {
   int64_t ldob;
   int f;
   int w256;                  // 1: lanes gather 32-byte column pairs with 256-bit loads (X 32-B aligned, ldx % 8 == 0)
+  int heavy_bucket;          // rows of degree bucket >= this are CTA-split ("heavy"; the first of perm)
+  int hseg;                  // 1: heavy rows as warp segments (htask) instead of CTA-split rows
+  const int4* __restrict__ htask;      // heavy-row segments (normalize): row, k_begin, k_end, first
+  const int32_t* __restrict__ hcount;  // segments of the row whose first segment is the index
+  const int32_t* __restrict__ n_hseg_ptr;
+  float4* __restrict__ hseg_ws;        // [segment][f4] partial sums of multi-segment rows
+  int* __restrict__ hseg_ctr;          // [first segment][chunk] arrival counters (zero between launches)
 };
 
 constexpr int kWarps = 8;
@@ -289,16 +296,108 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
   __shared__ float4 part[kWarps][32 * V];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int n_heavy = *a.n_heavy_ptr;
+  // heavy rows for this launch: degree buckets >= heavy_bucket (perm leads with them)
+  int n_heavy;
+  {
+    const int c = lane < kBins && lane >= a.heavy_bucket ? a.bucket_counts[lane] : 0;
+    n_heavy = __reduce_add_sync(0xffffffffu, c);
+  }
   const int n_light = a.n - n_heavy;
   int2* st = stage[warp];
+
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t GW = (int64_t)gridDim.x * kWarps;
+  if (a.hseg == 1 || (a.hseg == 2 && *a.n_mega_ptr > 0)) {
+    // One warp task per (heavy-row segment | light row, chunk), chunk-major, the segments (each
+    // <= kHSeg neighbors, the longest tasks) first, then the light rows by descending degree.
+    // A heavy row's segments write their partial sums to the workspace; the row's last segment
+    // to arrive (per-(row, chunk) counter) adds the partials in segment order and runs the
+    // epilogue -- deterministic, and no CTA barrier anywhere (a CTA-split row of degree 260
+    // gathers 14 % (f = 1024) / 25 % (f = 200) slower than a degree-250 row handled by one warp;
+    // as two segments it recovers a third to half of that: tools/spmm_degree_bench.py).
+    const int hs = *a.n_hseg_ptr;
+    const int64_t per = (int64_t)hs + n_light;
+    const int64_t L = per * a.nchunks;
+    for (int64_t t = gw; t < L; t += GW) {
+      const int chunk = (int)(t / per);
+      const int r = (int)(t % per);
+      const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
+      int row, b, e, first = -1, cnt = 1;
+      if (r < hs) {
+        const int4 ht = __ldg(a.htask + r);
+        row = ht.x; b = ht.y; e = ht.z; first = ht.w;
+        cnt = __ldg(a.hcount + first);
+      } else {
+        row = a.perm[n_heavy + (r - hs)];
+        b = a.rowptr[row];
+        e = a.rowptr[row + 1];
+      }
+      uint32_t mw0 = 0, mw1 = 0;  // gate words, loaded before the gathers
+      if (a.mbits) {
+        const uint32_t* mr = a.mbits + (int64_t)row * a.ldmb;
+        const int g0 = W256 ? c0 + 2 * lane : c0 + lane;
+        if (g0 < lim) mw0 = __ldg(mr + (g0 >> 3));
+        if (!W256 && g0 + 32 < lim) mw1 = __ldg(mr + ((g0 + 32) >> 3));
+      }
+      int c4, c4b;
+      Acc A;
+      if (W256) {
+        c4 = c0 + 2 * lane;
+        c4b = c4 + 1;
+        warp_row_sum256<UU>(a, st, b, e, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
+      } else {
+        c4 = c0 + lane;
+        c4b = c4 + 32;
+        if (a.cw == 32 * V && lim == (chunk + 1) * a.cw)
+          warp_row_sum<true>(a, st, b, e, 16u * c4, 16u * (c4 + 32), lane, A);
+        else
+          warp_row_sum<false>(a, st, b, e, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
+      }
+      const bool act0 = c4 < lim, act1 = c4b < lim;
+      if (cnt == 1) {
+        if (act0) store_row(a, row, c4, acc_part(A, 0), &mw0);
+        if (act1) store_row(a, row, c4b, acc_part(A, 1), W256 ? &mw0 : &mw1);
+        continue;
+      }
+      float4* ws = a.hseg_ws + (int64_t)r * a.f4;
+      if (act0) __stcg(ws + c4, acc_part(A, 0));
+      if (act1) __stcg(ws + c4b, acc_part(A, 1));
+      __threadfence();
+      __syncwarp();
+      int prev = 0;
+      if (lane == 0) prev = atomicAdd(a.hseg_ctr + (int64_t)first * a.nchunks + chunk, 1);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev == cnt - 1) {  // the row's last segment: combine in segment order
+        __threadfence();
+        const float4* w0 = a.hseg_ws + (int64_t)first * a.f4;
+        if (act0) {
+          float4 tot = __ldcg(w0 + c4);
+          for (int g = 1; g < cnt; g++) {
+            const float4 p = __ldcg(w0 + (int64_t)g * a.f4 + c4);
+            tot.x += p.x; tot.y += p.y; tot.z += p.z; tot.w += p.w;
+          }
+          store_row(a, row, c4, tot, &mw0);
+        }
+        if (act1) {
+          float4 tot = __ldcg(w0 + c4b);
+          for (int g = 1; g < cnt; g++) {
+            const float4 p = __ldcg(w0 + (int64_t)g * a.f4 + c4b);
+            tot.x += p.x; tot.y += p.y; tot.z += p.z; tot.w += p.w;
+          }
+          store_row(a, row, c4b, tot, W256 ? &mw0 : &mw1);
+        }
+        if (lane == 0) a.hseg_ctr[(int64_t)first * a.nchunks + chunk] = 0;  // ready for the next launch
+      }
+    }
+    return;
+  }
 
   // ---- phase 1: heavy rows, one CTA per (row, chunk), neighbors split across 8 warps; the
   // mega rows (deg' >= kMegaMinDeg, the first n_mega of perm) additionally split over kMegaSegs
   // CTAs per chunk: each writes its CTA-reduced partial to the workspace and the last of the
   // row's segments to arrive (per-(row, chunk) counter) sums them in segment order and stores
   // (deterministic) -- a 4.5K-degree row no longer serializes ~560 neighbors per warp.
-  const int n_mega = min(*a.n_mega_ptr, a.cap_mega);
+  const int n_mega = min(min(*a.n_mega_ptr, a.cap_mega), n_heavy);
   const int64_t HM = (int64_t)n_mega * kMegaSegs * a.nchunks;
   const int64_t H = HM + (int64_t)(n_heavy - n_mega) * a.nchunks;
   for (int64_t t = blockIdx.x; t < H; t += gridDim.x) {
@@ -388,8 +487,6 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
 
   // ---- phase 2: light rows, one warp per (row, chunk) ----
   const int64_t L = (int64_t)n_light * a.nchunks;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
-  const int64_t GW = (int64_t)gridDim.x * kWarps;
   for (int64_t t = gw; t < L; t += GW) {
     const int chunk = (int)(t / n_light);
     const int row = a.perm[n_heavy + (int)(t % n_light)];
@@ -573,6 +670,28 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
         a.mega_ws = static_cast<float4*>(ctx->ws_mega.ptr);
         a.mega_ctr = static_cast<int*>(ctx->ws_megactr.ptr);
       }
+    }
+    // heavy rows as warp segments (GSG_SPMM_HSEG=0: the CTA-split heavy phase, A/B)
+    static const int hseg_env = getenv("GSG_SPMM_HSEG") ? atoi(getenv("GSG_SPMM_HSEG")) : 1;
+    // Warp segments beat CTA-split heavy rows for narrow launches (f <= 512: config 3-5 f = 200
+    // 36.2 -> 33.0 / 50.8 -> 48.2 / 120.6 -> 116.8 us) and where mega rows exist (config 4
+    // f = 1024 180 -> 166 us), but not for the f = 1024 launches of graphs without them (config 5
+    // 522 -> 529, config 3 107 -> 109 us): hseg = 2 lets the kernel decide from the device-side
+    // mega-row count. profiles/r02_spmm_hseg_ab.txt
+    a.heavy_bucket = 32 - __builtin_clz((unsigned)kHeavyMinDeg);
+    a.hseg = (hseg_env && sg->htask) ? (a.nchunks >= 4 ? 2 : 1) : 0;
+    if (a.hseg) {
+      const size_t cap = sg->cap_hseg;
+      if (int rc = ctx->ws_hseg.reserve(sizeof(float4) * cap * a.f4)) return rc;
+      const size_t had = ctx->ws_hsegctr.bytes;
+      if (int rc = ctx->ws_hsegctr.reserve(sizeof(int) * cap * a.nchunks)) return rc;
+      if (ctx->ws_hsegctr.bytes != had)
+        GSG_CUDA(cudaMemsetAsync(ctx->ws_hsegctr.ptr, 0, ctx->ws_hsegctr.bytes, ctx->stream));
+      a.htask = sg->htask;
+      a.hcount = sg->hcount;
+      a.n_hseg_ptr = sg->counters + kNHSeg;
+      a.hseg_ws = static_cast<float4*>(ctx->ws_hseg.ptr);
+      a.hseg_ctr = static_cast<int*>(ctx->ws_hsegctr.ptr);
     }
     a.cw = (a.f4 + a.nchunks - 1) / a.nchunks;
     static const int w256_env = getenv("GSG_SPMM_W256") ? atoi(getenv("GSG_SPMM_W256")) : 1;
