@@ -8,6 +8,10 @@ namespace {
 
 __device__ __forceinline__ int bucket_of(int d) { return d <= 0 ? 0 : 32 - __clz(d); }
 
+__global__ void k_zero(int32_t* __restrict__ p, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = 0;
+}
+
 // One warp per row: rowptr[i] = indptr[i] + self*i, the degree-bucket histogram and max
 // degree, the per-row value of the degree modes (rowval[i] = fp32(1/(d_i+1)) row-self or
 // fp32(1/d_i) row, reused by k_fill for Â_ij and, gathered at column j, for Âᵀ_ij = Â_ji),
@@ -129,7 +133,7 @@ __global__ void k_transpose_vals(int n, const int32_t* __restrict__ rowptr, cons
 // with one global atomic per (block, bucket) on a zeroed cursor (the order within a bucket is
 // immaterial: every row is summed by one warp or CTA in CSR order).
 __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t* __restrict__ counters,
-                              int32_t* __restrict__ perm) {
+                              int32_t* __restrict__ perm, int4* __restrict__ htask, int32_t* __restrict__ hcount) {
   __shared__ int cnt[kBins], base[kBins], off[kBins];
   if (threadIdx.x == 0) {
     int acc = 0, heavy = 0, mega = 0;
@@ -152,8 +156,18 @@ __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t
     const int i = i0 + threadIdx.x;
     int b = -1, r = 0;
     if (i < n) {
-      b = bucket_of(rowptr[i + 1] - rowptr[i]);
+      const int rb = rowptr[i], d = rowptr[i + 1] - rb;
+      b = bucket_of(d);
       r = atomicAdd(&cnt[b], 1);
+      if (htask && d >= kHeavyMinDeg) {
+        // the heavy row's warp segments for the SpMM: ceil(d / kHSeg) equal pieces, contiguous
+        // in htask at a place reserved by one atomic (the order of rows in the list is
+        // immaterial: each row's partial sums are combined in segment order)
+        const int sc = (d + kHSeg - 1) / kHSeg, len = (d + sc - 1) / sc;
+        const int first = atomicAdd(&counters[kNHSeg], sc);
+        hcount[first] = sc;
+        for (int s2 = 0; s2 < sc; s2++) htask[first + s2] = make_int4(i, rb + s2 * len, min(rb + d, rb + (s2 + 1) * len), first);
+      }
     }
     __syncthreads();
     if (threadIdx.x < kBins && cnt[threadIdx.x])
@@ -162,48 +176,6 @@ __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t
     if (b >= 0) perm[base[b] + r] = i;
     __syncthreads();
   }
-}
-
-// Heavy rows (the first n_heavy of perm, deg' >= kHeavyMinDeg) cut into ceil(deg' / kHSeg)
-// equal warp segments, listed in perm order: htask[s] = (row, k_begin, k_end, first segment of
-// the row), hcount[first] = the row's segment count; counters[kNHSeg] = the number of segments.
-// One block: an exclusive scan of the per-row counts over n_heavy rows, 1024 at a time.
-__global__ void k_heavy_tasks(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ perm,
-                              int32_t* __restrict__ counters, int4* __restrict__ htask, int32_t* __restrict__ hcount) {
-  __shared__ int scan[1024];
-  __shared__ int base;
-  const int n_heavy = counters[kBins];
-  if (threadIdx.x == 0) base = 0;
-  __syncthreads();
-  for (int r0 = 0; r0 < n_heavy; r0 += blockDim.x) {
-    const int i = r0 + threadIdx.x;
-    int row = 0, b = 0, d = 0, cnt = 0;
-    if (i < n_heavy) {
-      row = perm[i];
-      b = rowptr[row];
-      d = rowptr[row + 1] - b;
-      cnt = (d + kHSeg - 1) / kHSeg;
-    }
-    scan[threadIdx.x] = cnt;
-    __syncthreads();
-    for (int off = 1; off < (int)blockDim.x; off <<= 1) {  // inclusive Hillis-Steele scan
-      const int v = threadIdx.x >= (unsigned)off ? scan[threadIdx.x - off] : 0;
-      __syncthreads();
-      scan[threadIdx.x] += v;
-      __syncthreads();
-    }
-    const int first = base + scan[threadIdx.x] - cnt;
-    if (i < n_heavy) {
-      const int len = (d + cnt - 1) / cnt;  // equal segments of <= kHSeg neighbors
-      hcount[first] = cnt;
-      for (int s = 0; s < cnt; s++)
-        htask[first + s] = make_int4(row, b + s * len, min(b + d, b + (s + 1) * len), first);
-    }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) base += scan[threadIdx.x];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) counters[kNHSeg] = base;
 }
 
 }  // namespace
@@ -239,7 +211,10 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
     }
   }
   ProfScope ps(ctx, GSG_K_NORM, 16.0 * nh + 24.0 * n, 0.0);
-  GSG_CUDA(cudaMemsetAsync(sg->counters, 0, sizeof(int32_t) * (3 * kBins + 8), st));
+  // counters zeroed by a kernel, not a memset node: inside the step's CUDA graph a memset
+  // node cost ~7.5 us of idle time before the next kernel (r02 timeline), a kernel < 1 us
+  k_zero<<<1, 128, 0, st>>>(sg->counters, 3 * kBins + 8);
+  count_launch(ctx);
   const int T = 256;
   int grid = (n + 1 + T - 1) / T;
   if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
@@ -263,9 +238,8 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
       k_transpose_vals<<<wgrid, T, 0, st>>>(n, sg->rowptr, sg->col, sg->val, sg->valT, sg->counters + 3 * kBins + 4);
       count_launch(ctx);
     }
-    k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm);
-    k_heavy_tasks<<<1, 1024, 0, st>>>(sg->rowptr, sg->perm, sg->counters, sg->htask, sg->hcount);
-    count_launch(ctx, 2);
+    k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm, sg->htask, sg->hcount);
+    count_launch(ctx);
   }
   GSG_CUDA(cudaGetLastError());
   return GSG_OK;
