@@ -11,6 +11,7 @@
 // neighbor list with ballots -- rows come out ascending because the parent rows are ascending
 // and the rank map is monotone (the precondition of Alg. 4).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -305,6 +306,157 @@ __global__ void k_induce_fill(const int64_t* __restrict__ indptr, const int32_t*
   }
 }
 
+// Induction with the sampler's V_s bitmap in SHARED memory (one 1024-thread block per sample):
+// the global-bitmap kernels above test every parent neighbor of every sampled node against a
+// 200 KB-per-sample bitmap that, for hundreds of samples, no longer fits the L2 (2/3 of a
+// sampling call went there). Count pass: per-row hit counts, then the exclusive scan into the
+// sample's indptr. Fill pass: the same scan writing local ids, ranked through a uint16 prefix per
+// 4-word group (local ids < 65536) plus at most 3 word popcounts. Used when the bitmap and the
+// group prefixes fit in shared memory (parents up to ~1.6M nodes) and n < 65536.
+constexpr int kInduceThreads = 1024;
+
+__device__ __forceinline__ void load_bitmap_smem(const uint32_t* __restrict__ bits, int64_t words, uint32_t* sb) {
+  for (int64_t w = threadIdx.x; w < words; w += blockDim.x) sb[w] = bits[w];
+}
+
+__device__ __forceinline__ bool sbit(const uint32_t* sb, int32_t v) { return (sb[v >> 5] >> (v & 31)) & 1u; }
+
+__global__ void __launch_bounds__(kInduceThreads) k_induce_count_smem(const int64_t* __restrict__ indptr,
+                                                                      const int32_t* __restrict__ indices,
+                                                                      const uint32_t* __restrict__ bitmaps, int64_t words,
+                                                                      const int32_t* __restrict__ nodes_all,
+                                                                      const int32_t* __restrict__ nv, int n_cap,
+                                                                      int32_t* __restrict__ rowcnt_all,
+                                                                      int64_t* __restrict__ indptr_all) {
+  extern __shared__ uint32_t sb[];
+  __shared__ int64_t part[32];
+  const int s = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  load_bitmap_smem(bitmaps + (int64_t)s * words, words, sb);
+  __syncthreads();
+  const int n = nv[s];
+  const int32_t* nodes = nodes_all + (int64_t)s * n_cap;
+  int32_t* rc = rowcnt_all + (int64_t)s * n_cap;
+  for (int i = warp; i < n; i += kInduceThreads / 32) {
+    const int32_t v = nodes[i];
+    const int64_t b = indptr[v], e = indptr[v + 1];
+    int c = 0;
+    for (int64_t k0 = b; k0 < e; k0 += 128) {  // 4 independent loads per lane in flight
+      int32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) w[q] = k0 + 32 * q + lane < e ? indices[k0 + 32 * q + lane] : -1;
+#pragma unroll
+      for (int q = 0; q < 4; q++) c += __popc(__ballot_sync(0xffffffffu, w[q] >= 0 && sbit(sb, w[q])));
+    }
+    if (lane == 0) rc[i] = c;
+  }
+  __syncthreads();
+  // indptr = exclusive scan of the row counts (rows split into equal runs per thread)
+  int64_t* ip = indptr_all + (int64_t)s * (n_cap + 1);
+  const int per = (n + kInduceThreads - 1) / kInduceThreads;
+  const int r0 = threadIdx.x * per, r1 = min(n, r0 + per);
+  int64_t sum = 0;
+  for (int r = r0; r < r1; r++) sum += rc[r];
+  int64_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) part[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t t = part[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += u;
+    }
+    part[lane] = t;
+  }
+  __syncthreads();
+  int64_t run = (warp > 0 ? part[warp - 1] : 0) + incl - sum;
+  for (int r = r0; r < r1; r++) {
+    ip[r] = run;
+    run += rc[r];
+  }
+  if (threadIdx.x == 0) ip[n] = part[31];
+}
+
+__global__ void __launch_bounds__(kInduceThreads) k_induce_fill_smem(const int64_t* __restrict__ indptr,
+                                                                     const int32_t* __restrict__ indices,
+                                                                     const uint32_t* __restrict__ bitmaps, int64_t words,
+                                                                     const int32_t* __restrict__ nodes_all,
+                                                                     const int32_t* __restrict__ nv, int n_cap,
+                                                                     const int64_t* __restrict__ sub_indptr_all,
+                                                                     const int64_t* __restrict__ idx_off,
+                                                                     int32_t* __restrict__ sub_indices) {
+  extern __shared__ uint32_t sb[];
+  __shared__ int32_t part[32];
+  const int s = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  load_bitmap_smem(bitmaps + (int64_t)s * words, words, sb);
+  uint16_t* gp = reinterpret_cast<uint16_t*>(sb + words);  // [ceil(words / 4)] rank before each 4-word group
+  const int64_t groups = (words + 3) / 4;
+  __syncthreads();
+  {  // group prefixes: each thread a contiguous run of groups, block scan of the run sums
+    const int64_t per = (groups + kInduceThreads - 1) / kInduceThreads;
+    const int64_t g0 = threadIdx.x * per, g1 = min(groups, g0 + per);
+    int32_t sum = 0;
+    for (int64_t g = g0; g < g1; g++)
+      for (int64_t w = 4 * g; w < min(words, 4 * g + 4); w++) sum += __popc(sb[w]);
+    int32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) part[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t t = part[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t u = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += u;
+      }
+      part[lane] = t;
+    }
+    __syncthreads();
+    int32_t run = (warp > 0 ? part[warp - 1] : 0) + incl - sum;
+    for (int64_t g = g0; g < g1; g++) {
+      gp[g] = (uint16_t)run;
+      for (int64_t w = 4 * g; w < min(words, 4 * g + 4); w++) run += __popc(sb[w]);
+    }
+  }
+  __syncthreads();
+  const int n = nv[s];
+  const int32_t* nodes = nodes_all + (int64_t)s * n_cap;
+  const int64_t* sip = sub_indptr_all + (int64_t)s * (n_cap + 1);
+  int32_t* outb = sub_indices + idx_off[s];
+  for (int i = warp; i < n; i += kInduceThreads / 32) {
+    const int32_t v = nodes[i];
+    const int64_t b = indptr[v], e = indptr[v + 1];
+    int32_t* out = outb + sip[i];
+    int o = 0;
+    for (int64_t k0 = b; k0 < e; k0 += 128) {
+      int32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) w[q] = k0 + 32 * q + lane < e ? indices[k0 + 32 * q + lane] : -1;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const bool hit = w[q] >= 0 && sbit(sb, w[q]);
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int32_t wd = w[q] >> 5;
+          int32_t r = gp[wd >> 2];
+          for (int32_t x = wd & ~3; x < wd; x++) r += __popc(sb[x]);
+          out[o + __popc(m & ((1u << lane) - 1))] = r + __popc(sb[wd] & ((1u << (w[q] & 31)) - 1));
+        }
+        o += __popc(m);
+      }
+    }
+  }
+}
+
 // gsg_sample_load: sample *d_k into a device-sized subgraph of n_pad nodes. Nodes n_k .. n_pad-1
 // are isolated padding (empty rows; normalization gives them a self loop, their feature rows are
 // gathered as zeros and their loss weight is 0), so one CUDA graph of the step serves every
@@ -443,10 +595,25 @@ GSG_API int gsg_frontier_sample(gsg_ctx_t c, gsg_parent_t p, int32_t n, int32_t 
   const int64_t warps = (int64_t)count * n;
   int grid = (int)std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)c->num_sms * 16);
   // row counts reuse the V_s insertion-order buffer (no longer needed after k_rank)
-  k_rowcount<<<grid, 256, 0, st>>>(p->indptr, p->indices, (const uint32_t*)bitmaps.ptr, words, S->nodes,
-                                   (const int32_t*)nv.ptr, count, n, (int32_t*)vs.ptr);
-  k_rowscan<<<count, 1024, 0, st>>>(n, (const int32_t*)nv.ptr, (const int32_t*)vs.ptr, S->indptr);
-  count_launch(c, 4);
+  // shared-memory induction when the V_s bitmap (+ uint16 group prefixes) fits one block
+  const size_t ind_smem = sizeof(uint32_t) * (size_t)words + sizeof(uint16_t) * (size_t)((words + 3) / 4) + 16;
+  static const int ind_env = getenv("GSG_SAMPLER_SMEM_INDUCE") ? atoi(getenv("GSG_SAMPLER_SMEM_INDUCE")) : 1;
+  const bool smem_ind = ind_env && n < 65536 && ind_smem <= 225u * 1024u;
+  if (smem_ind) {
+    e = cudaFuncSetAttribute(k_induce_count_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ind_smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_induce_fill_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ind_smem);
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaFuncSetAttribute(induce)"));
+    k_induce_count_smem<<<count, kInduceThreads, ind_smem, st>>>(p->indptr, p->indices, (const uint32_t*)bitmaps.ptr,
+                                                                  words, S->nodes, (const int32_t*)nv.ptr, n,
+                                                                  (int32_t*)vs.ptr, S->indptr);
+    count_launch(c, 3);
+  } else {
+    k_rowcount<<<grid, 256, 0, st>>>(p->indptr, p->indices, (const uint32_t*)bitmaps.ptr, words, S->nodes,
+                                     (const int32_t*)nv.ptr, count, n, (int32_t*)vs.ptr);
+    k_rowscan<<<count, 1024, 0, st>>>(n, (const int32_t*)nv.ptr, (const int32_t*)vs.ptr, S->indptr);
+    count_launch(c, 4);
+  }
   if ((e = cudaGetLastError()) != cudaSuccess) return cleanup(cuda_fail(e, "sampler kernels"));
   // size the induced CSR arrays (the one host synchronization)
   S->n_k.resize(count);
@@ -472,9 +639,14 @@ GSG_API int gsg_frontier_sample(gsg_ctx_t c, gsg_parent_t p, int32_t n, int32_t 
   if (e == cudaSuccess) e = cudaMemcpyAsync(S->d_idx_off, S->idx_off.data(), sizeof(int64_t) * count, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(S->d_n, nv.ptr, sizeof(int32_t) * count, cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(sample indices)"));
-  k_induce_fill<<<grid, 256, 0, st>>>(p->indptr, p->indices, (const uint32_t*)bitmaps.ptr, words,
-                                      (const int32_t*)wordpre.ptr, S->nodes, (const int32_t*)nv.ptr, count, n,
-                                      S->indptr, S->d_idx_off, S->indices);
+  if (smem_ind)
+    k_induce_fill_smem<<<count, kInduceThreads, ind_smem, st>>>(p->indptr, p->indices, (const uint32_t*)bitmaps.ptr,
+                                                                 words, S->nodes, (const int32_t*)nv.ptr, n, S->indptr,
+                                                                 S->d_idx_off, S->indices);
+  else
+    k_induce_fill<<<grid, 256, 0, st>>>(p->indptr, p->indices, (const uint32_t*)bitmaps.ptr, words,
+                                        (const int32_t*)wordpre.ptr, S->nodes, (const int32_t*)nv.ptr, count, n,
+                                        S->indptr, S->d_idx_off, S->indices);
   count_launch(c);
   e = cudaStreamSynchronize(st);
   bitmaps.release(); vs.release(); nv.release(); wordpre.release();
