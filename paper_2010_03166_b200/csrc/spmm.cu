@@ -77,6 +77,7 @@ constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int V = 2;   // float4 per lane per neighbor (full-warp path)
 constexpr int U = 8;   // neighbors per unrolled iteration
+constexpr int kRing = 1;  // heavy-row tasks whose partial sums a CTA holds at once
 
 // acc += a * x on packed fp32 pairs (FFMA2, round-to-nearest per element: identical to two FFMAs)
 __device__ __forceinline__ void fma2(float2& acc, float a, float2 x) {
@@ -293,9 +294,16 @@ __device__ __forceinline__ float4 acc_part(const Acc& A, int q) {
 template <int MINB, bool W256, int UU = U>
 __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
   __shared__ __align__(16) int2 stage[kWarps][40];
-  __shared__ float4 part[kWarps][32 * V];
+  __shared__ float4 part[kRing][kWarps][32 * V];  // heavy rows: per-warp partial sums, kRing tasks deep
+  __shared__ int ring_arrive[kRing];              // warps that have written a slot's partials
+  __shared__ int ring_gen[kRing];                 // reductions completed per slot (slot reuse)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  if (threadIdx.x < kRing) {
+    ring_arrive[threadIdx.x] = 0;
+    ring_gen[threadIdx.x] = 0;
+  }
+  __syncthreads();
   // heavy rows for this launch: degree buckets >= heavy_bucket (perm leads with them)
   int n_heavy;
   {
@@ -397,10 +405,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
   // CTAs per chunk: each writes its CTA-reduced partial to the workspace and the last of the
   // row's segments to arrive (per-(row, chunk) counter) sums them in segment order and stores
   // (deterministic) -- a 4.5K-degree row no longer serializes ~560 neighbors per warp.
+  // No CTA barrier per task: every warp writes its partial sums into the task's ring slot and the
+  // LAST warp to arrive (shared-memory counter) reduces them in warp order -- the same fixed
+  // order as a barrier-synchronized reduction -- while the other warps go on to their next task
+  // (a slot is reused kRing tasks later, once its reduction has released it).
   const int n_mega = min(min(*a.n_mega_ptr, a.cap_mega), n_heavy);
   const int64_t HM = (int64_t)n_mega * kMegaSegs * a.nchunks;
   const int64_t H = HM + (int64_t)(n_heavy - n_mega) * a.nchunks;
-  for (int64_t t = blockIdx.x; t < H; t += gridDim.x) {
+  int task_i = 0;
+  for (int64_t t = blockIdx.x; t < H; t += gridDim.x, task_i++) {
+    const int slot = task_i % kRing, gen = task_i / kRing;
     int chunk, row, sgi = -1, m = 0;
     if (t < HM) {
       chunk = (int)(t / ((int64_t)n_mega * kMegaSegs));
@@ -437,17 +451,25 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
         warp_row_sum<false>(a, st, w0, w1, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
     }
     const bool act0 = c4 < lim, act1 = c4b < lim;
-    part[warp][lane] = acc_part(A, 0);
-    part[warp][lane + 32] = acc_part(A, 1);
-    __syncthreads();
-    if (warp == 0) {
+    while (*reinterpret_cast<volatile int*>(&ring_gen[slot]) < gen) {
+    }  // the slot's previous task has been reduced
+    part[slot][warp][lane] = acc_part(A, 0);
+    part[slot][warp][lane + 32] = acc_part(A, 1);
+    __threadfence_block();
+    __syncwarp();
+    int arrived = 0;
+    if (lane == 0) arrived = atomicAdd(&ring_arrive[slot], 1);
+    arrived = __shfl_sync(0xffffffffu, arrived, 0);
+    if (arrived == kWarps - 1) {  // the last warp of this task reduces it
+      __threadfence_block();
+      if (lane == 0) ring_arrive[slot] = 0;
       float4 s[V];
 #pragma unroll
       for (int q = 0; q < V; q++) {
-        s[q] = part[0][lane + 32 * q];
+        s[q] = part[slot][0][lane + 32 * q];
 #pragma unroll
         for (int w = 1; w < kWarps; w++) {
-          const float4 p = part[w][lane + 32 * q];
+          const float4 p = part[slot][w][lane + 32 * q];
           s[q].x += p.x; s[q].y += p.y; s[q].z += p.z; s[q].w += p.w;
         }
       }
@@ -481,8 +503,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
           if (lane == 0) a.mega_ctr[(int64_t)m * a.nchunks + chunk] = 0;  // ready for the next launch
         }
       }
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) *reinterpret_cast<volatile int*>(&ring_gen[slot]) = gen + 1;  // release the slot
     }
-    __syncthreads();
   }
 
   // ---- phase 2: light rows, one warp per (row, chunk) ----
