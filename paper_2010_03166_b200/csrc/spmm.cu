@@ -65,6 +65,7 @@ struct SpmmArgs {
   int f;
   int w256;                  // 1: lanes gather 32-byte column pairs with 256-bit loads (X 32-B aligned, ldx % 8 == 0)
   int heavy_bucket;          // rows of degree bucket >= this are CTA-split ("heavy"; the first of perm)
+  int seg_align;             // CTA-split rows: each warp's share rounded up to a multiple of this
   int hseg;                  // 1: heavy rows as warp segments (htask) instead of CTA-split rows
   const int4* __restrict__ htask;      // heavy-row segments (normalize): row, k_begin, k_end, first
   const int32_t* __restrict__ hcount;  // segments of the row whose first segment is the index
@@ -433,7 +434,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
       b = min(e, b + sgi * sl);
       e = min(e, b + sl);
     }
-    const int seg = (e - b + kWarps - 1) / kWarps;
+    int seg = (e - b + kWarps - 1) / kWarps;
+    seg = (seg + a.seg_align - 1) / a.seg_align * a.seg_align;
     const int w0 = min(e, b + warp * seg), w1 = min(e, w0 + seg);
     const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
     int c4, c4b;  // output float4 columns of acc_part(A, 0) and acc_part(A, 1)
@@ -703,6 +705,11 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
     // 522 -> 529, config 3 107 -> 109 us): hseg = 2 lets the kernel decide from the device-side
     // mega-row count. profiles/r02_spmm_hseg_ab.txt
     a.heavy_bucket = 32 - __builtin_clz((unsigned)kHeavyMinDeg);
+    // a CTA-split row's per-warp shares in multiples of 8 neighbors (one batch): no partial batch
+    // inside a row; the last warps take the remainder, and with no barrier per task an idle warp
+    // moves on (config 5 f = 1024 515.7 -> 510.4 us; 32 slower; profiles/r02_spmm_heavy_ring_ab.txt)
+    static const int align_env = getenv("GSG_SPMM_SEG_ALIGN") ? atoi(getenv("GSG_SPMM_SEG_ALIGN")) : 8;
+    a.seg_align = std::max(1, align_env);
     a.hseg = (hseg_env && sg->htask) ? (a.nchunks >= 4 ? 2 : 1) : 0;
     if (a.hseg) {
       const size_t cap = sg->cap_hseg;
