@@ -710,7 +710,8 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
     // moves on (config 5 f = 1024 515.7 -> 510.4 us; 32 slower; profiles/r02_spmm_heavy_ring_ab.txt)
     static const int align_env = getenv("GSG_SPMM_SEG_ALIGN") ? atoi(getenv("GSG_SPMM_SEG_ALIGN")) : 8;
     a.seg_align = std::max(1, align_env);
-    a.hseg = (hseg_env && sg->htask) ? (a.nchunks >= 4 ? 2 : 1) : 0;
+    // GSG_SPMM_HSEG (A/B): 0 never, 2 always, 3 only where mega rows exist (at every width)
+    a.hseg = (hseg_env && sg->htask) ? (hseg_env == 2 || (hseg_env == 1 && a.nchunks < 4) ? 1 : 2) : 0;
     if (a.hseg) {
       const size_t cap = sg->cap_hseg;
       if (int rc = ctx->ws_hseg.reserve(sizeof(float4) * cap * a.f4)) return rc;
