@@ -305,10 +305,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
     ring_gen[threadIdx.x] = 0;
   }
   __syncthreads();
-  // heavy rows for this launch: degree buckets >= heavy_bucket (perm leads with them)
+  // heavy rows for this launch: degree buckets >= heavy_bucket (perm leads with them); the warp
+  // segments (htask, built by normalize) cover exactly the rows of deg' >= kHeavyMinDeg
+  const bool segs = a.hseg == 1 || (a.hseg == 2 && *a.n_mega_ptr > 0);
+  const int hbkt = segs ? 32 - __clz(kHeavyMinDeg) : a.heavy_bucket;
   int n_heavy;
   {
-    const int c = lane < kBins && lane >= a.heavy_bucket ? a.bucket_counts[lane] : 0;
+    const int c = lane < kBins && lane >= hbkt ? a.bucket_counts[lane] : 0;
     n_heavy = __reduce_add_sync(0xffffffffu, c);
   }
   const int n_light = a.n - n_heavy;
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
 
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
   const int64_t GW = (int64_t)gridDim.x * kWarps;
-  if (a.hseg == 1 || (a.hseg == 2 && *a.n_mega_ptr > 0)) {
+  if (segs) {
     // One warp task per (heavy-row segment | light row, chunk), chunk-major, the segments (each
     // <= kHSeg neighbors, the longest tasks) first, then the light rows by descending degree.
     // A heavy row's segments write their partial sums to the workspace; the row's last segment
@@ -704,7 +707,8 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
     // f = 1024 180 -> 166 us), but not for the f = 1024 launches of graphs without them (config 5
     // 522 -> 529, config 3 107 -> 109 us): hseg = 2 lets the kernel decide from the device-side
     // mega-row count. profiles/r02_spmm_hseg_ab.txt
-    a.heavy_bucket = 32 - __builtin_clz((unsigned)kHeavyMinDeg);
+    static const int hb_env = getenv("GSG_SPMM_HEAVY_BUCKET") ? atoi(getenv("GSG_SPMM_HEAVY_BUCKET")) : 0;  // A/B
+    a.heavy_bucket = hb_env > 0 ? hb_env : 32 - __builtin_clz((unsigned)kHeavyMinDeg);
     // a CTA-split row's per-warp shares in multiples of 8 neighbors (one batch): no partial batch
     // inside a row; the last warps take the remainder, and with no barrier per task an idle warp
     // moves on (config 5 f = 1024 515.7 -> 510.4 us; 32 slower; profiles/r02_spmm_heavy_ring_ab.txt)
