@@ -356,7 +356,10 @@ GSG_API int gsg_parent_upload(gsg_ctx_t ctx, int64_t N, int64_t nnz, const int64
                               const int32_t* h_indices, gsg_parent_t* out);
 GSG_API int gsg_parent_free(gsg_parent_t parent);
 /* Sample and induce `count` subgraphs (sampler k uses seed_k above). 1 <= m <= n <= N, m <= 16384,
- * clip >= 1. Synchronizes the context stream once (to size the induced CSR arrays). */
+ * clip >= 1. Synchronizes the context stream once (to size the induced CSR arrays). The call's
+ * scratch (bitmaps, lists) stays with the context; the batch's arrays come from, and at
+ * gsg_sample_free go back to, a small pool of the context (a config-5 batch of 888 holds 8.3 GB
+ * of induced indices), so a sampling loop does not allocate per call. */
 GSG_API int gsg_frontier_sample(gsg_ctx_t ctx, gsg_parent_t parent, int32_t n, int32_t m,
                                 int32_t clip, uint64_t seed, int32_t count, gsg_sample_t* out);
 /* Device views of subgraph k (valid until gsg_sample_free): n_k nodes, nnz_k entries,
@@ -365,6 +368,8 @@ GSG_API int gsg_frontier_sample(gsg_ctx_t ctx, gsg_parent_t parent, int32_t n, i
 GSG_API int gsg_sample_get(gsg_sample_t s, int32_t k, int32_t* n_k, int64_t* nnz_k,
                            const int64_t** d_indptr, const int32_t** d_indices,
                            const int32_t** d_nodes);
+/* Releases the batch: a device-wide synchronization (as cudaFree), then its arrays return to the
+ * pool of the context that sampled it (or are freed, if that context was destroyed first). */
 GSG_API int gsg_sample_free(gsg_sample_t s);
 /* A subgraph whose sizes live on the device, so that one captured CUDA graph of the training
  * step serves every GPU-sampled subgraph (Alg. 7's pool refill, with Alg. 2 on the

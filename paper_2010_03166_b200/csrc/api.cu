@@ -238,6 +238,9 @@ GSG_API int gsg_ctx_destroy(gsg_ctx_t c) {
   c->ws_lp0.release(); c->ws_lp1.release(); c->ws_lp2.release(); c->ws_loss.release();
   c->ws_mega.release(); c->ws_megactr.release(); c->ws_hseg.release(); c->ws_hsegctr.release();
   for (int i = 0; i < 2; i++) { c->ws_x3[i].release(); c->ws_x3_side[i].release(); }
+  c->ws_sbits.release(); c->ws_svs.release(); c->ws_snv.release(); c->ws_swordpre.release(); c->ws_snnz.release();
+  gsg::sampler_detach(c);  // live samples keep their arrays and free them themselves
+  for (auto& b : c->spare) cudaFree(b.first);
   for (auto& r : c->prof.recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->prof.free_ev) cudaEventDestroy(e);
   if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
@@ -93,6 +94,8 @@ struct Profiler {
 };
 }  // namespace gsg
 
+struct gsg_sample;
+
 struct gsg_ctx {
   gsg::Profiler prof;
   int device = 0;
@@ -118,6 +121,12 @@ struct gsg_ctx {
   gsg::DevBuf ws_megactr;  // SpMM mega-row (row, chunk) arrival counters, zero between launches
   cudaStream_t side = nullptr;       // fork/join side stream (layer backward: dW next to T -> dX)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // gsg_frontier_sample: scratch of a call (V_s bitmaps, insertion lists, sizes) and the device
+  // arrays of freed sample batches kept for the next call -- a config-5 batch of 888 holds
+  // 8.3 GB of induced indices, and allocating / freeing that per call cost 2-500 ms of host time
+  gsg::DevBuf ws_sbits, ws_svs, ws_snv, ws_swordpre, ws_snnz;
+  std::vector<std::pair<void*, size_t>> spare;  // device buffers of freed samples (ptr, bytes)
+  std::vector<gsg_sample*> live_samples;        // samples whose buffers return to `spare` when freed
 };
 
 struct gsg_subgraph {
@@ -217,4 +226,5 @@ int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh,
                 float* dZ, int64_t lddz, void* dZlp, int64_t lddzlp);
 int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64_t lds, const void* labels,
                      const float* node_w, float* dS, float* loss);
+void sampler_detach(gsg_ctx* ctx);  // gsg_ctx_destroy: live samples stop returning buffers to it
 }  // namespace gsg

@@ -29,6 +29,8 @@ struct gsg_parent {
 
 struct gsg_sample {
   int device = 0;
+  gsg_ctx* owner = nullptr;    // context whose spare pool receives the arrays at gsg_sample_free
+  size_t nodes_bytes = 0, indptr_bytes = 0, indices_bytes = 0;
   int count = 0, n_cap = 0;
   std::vector<int32_t> n_k;
   std::vector<int64_t> nnz_k, idx_off;
@@ -489,10 +491,17 @@ __global__ void __launch_bounds__(kInduceThreads) k_induce_fill_smem(const int64
         const bool hit = w[q] >= 0 && sbit(sb, w[q]);
         const unsigned m = __ballot_sync(0xffffffffu, hit);
         if (hit) {
-          const int32_t wd = w[q] >> 5;
+          // rank = the group's prefix + the bits below v in its 4-word group, read as ONE 16-byte
+          // load (the words past the bitmap's end that a last group may cover lie above v)
+          const int32_t wd = w[q] >> 5, j = wd & 3;
+          const uint4 g4 = reinterpret_cast<const uint4*>(sb)[wd >> 2];
+          const uint32_t below = (1u << (w[q] & 31)) - 1;
           int32_t r = gp[wd >> 2];
-          for (int32_t x = wd & ~3; x < wd; x++) r += __popc(sb[x]);
-          out[o + __popc(m & ((1u << lane) - 1))] = r + __popc(sb[wd] & ((1u << (w[q] & 31)) - 1));
+          r += j > 0 ? __popc(g4.x) : __popc(g4.x & below);
+          if (j >= 1) r += j > 1 ? __popc(g4.y) : __popc(g4.y & below);
+          if (j >= 2) r += j > 2 ? __popc(g4.z) : __popc(g4.z & below);
+          if (j >= 3) r += __popc(g4.w & below);
+          out[o + __popc(m & ((1u << lane) - 1))] = r;
         }
         o += __popc(m);
       }
@@ -547,6 +556,46 @@ __global__ void k_advance(int32_t* d_k, int count) { *d_k = (*d_k + 1) % count; 
 }  // namespace gsg
 
 using namespace gsg;
+
+namespace gsg {
+// A device buffer of at least `bytes` for a sample array: the smallest spare of the context that
+// fits and is not more than twice as large, else a fresh allocation.
+static cudaError_t pool_take(gsg_ctx* c, size_t bytes, void** out, size_t* got) {
+  int best = -1;
+  for (int i = 0; i < (int)c->spare.size(); i++) {
+    const size_t b = c->spare[i].second;
+    if (b >= bytes && b <= 2 * bytes + (1u << 20) && (best < 0 || b < c->spare[best].second)) best = i;
+  }
+  if (best >= 0) {
+    *out = c->spare[best].first;
+    *got = c->spare[best].second;
+    c->spare.erase(c->spare.begin() + best);
+    return cudaSuccess;
+  }
+  *got = bytes;
+  return cudaMalloc(out, bytes);
+}
+
+// Back to the context's spare list (at most kSpare buffers are kept: the smallest goes).
+static void pool_give(gsg_ctx* c, void* p, size_t bytes) {
+  constexpr size_t kSpare = 8;
+  if (!p) return;
+  if (!c) { cudaFree(p); return; }
+  c->spare.emplace_back(p, bytes);
+  if (c->spare.size() > kSpare) {
+    size_t m = 0;
+    for (size_t i = 1; i < c->spare.size(); i++)
+      if (c->spare[i].second < c->spare[m].second) m = i;
+    cudaFree(c->spare[m].first);
+    c->spare.erase(c->spare.begin() + m);
+  }
+}
+
+void sampler_detach(gsg_ctx* c) {
+  for (gsg_sample* s : c->live_samples) s->owner = nullptr;
+  c->live_samples.clear();
+}
+}  // namespace gsg
 
 extern "C" {
 
@@ -604,7 +653,8 @@ GSG_API int gsg_frontier_sample(gsg_ctx_t c, gsg_parent_t p, int32_t n, int32_t 
   DeviceGuard dg(c->device);
   cudaStream_t st = c->stream;
   const int64_t words = (p->N + 31) / 32;
-  DevBuf bitmaps, vs, nv, wordpre, nnzb;
+  // scratch of this call: context workspaces, grown on demand and kept
+  DevBuf &bitmaps = c->ws_sbits, &vs = c->ws_svs, &nv = c->ws_snv, &wordpre = c->ws_swordpre, &nnzb = c->ws_snnz;
   int rc;
   if ((rc = bitmaps.reserve(sizeof(uint32_t) * words * count))) return rc;
   if ((rc = vs.reserve(sizeof(int32_t) * (int64_t)n * count))) return rc;
@@ -613,15 +663,17 @@ GSG_API int gsg_frontier_sample(gsg_ctx_t c, gsg_parent_t p, int32_t n, int32_t 
   if ((rc = nnzb.reserve(sizeof(int64_t) * count))) return rc;
   auto* S = new gsg_sample;
   S->device = c->device;
+  S->owner = c;
+  c->live_samples.push_back(S);
   S->count = count;
   S->n_cap = n;
   auto cleanup = [&](int code) {
-    bitmaps.release(); vs.release(); nv.release(); wordpre.release(); nnzb.release();
     gsg_sample_free(S);
     return code;
   };
-  cudaError_t e = cudaMalloc(&S->nodes, sizeof(int32_t) * (int64_t)n * count);
-  if (e == cudaSuccess) e = cudaMalloc(&S->indptr, sizeof(int64_t) * (int64_t)(n + 1) * count);
+  cudaError_t e = pool_take(c, sizeof(int32_t) * (int64_t)n * count, (void**)&S->nodes, &S->nodes_bytes);
+  if (e == cudaSuccess)
+    e = pool_take(c, sizeof(int64_t) * (int64_t)(n + 1) * count, (void**)&S->indptr, &S->indptr_bytes);
   if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc(sample)"));
   e = cudaMemsetAsync(bitmaps.ptr, 0, sizeof(uint32_t) * words * count, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(S->indptr, 0, sizeof(int64_t) * (int64_t)(n + 1) * count, st);
@@ -684,7 +736,7 @@ GSG_API int gsg_frontier_sample(gsg_ctx_t c, gsg_parent_t p, int32_t n, int32_t 
     S->idx_off[k] = tot;
     tot += S->nnz_k[k];
   }
-  e = cudaMalloc(&S->indices, sizeof(int32_t) * (tot > 0 ? tot : 1));
+  e = pool_take(c, sizeof(int32_t) * (tot > 0 ? tot : 1), (void**)&S->indices, &S->indices_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&S->d_idx_off, sizeof(int64_t) * count);
   if (e == cudaSuccess) e = cudaMalloc(&S->d_n, sizeof(int32_t) * count);
   if (e == cudaSuccess) e = cudaMalloc(&S->d_err, sizeof(int32_t));
@@ -702,7 +754,6 @@ GSG_API int gsg_frontier_sample(gsg_ctx_t c, gsg_parent_t p, int32_t n, int32_t 
                                         S->indptr, S->d_idx_off, S->indices);
   count_launch(c);
   e = cudaStreamSynchronize(st);
-  bitmaps.release(); vs.release(); nv.release(); wordpre.release(); nnzb.release();
   if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) {
     gsg_sample_free(S);
     return cuda_fail(e, "k_induce_fill");
@@ -753,9 +804,16 @@ GSG_API int gsg_sample_check(gsg_sample_t s) {
 GSG_API int gsg_sample_free(gsg_sample_t s) {
   if (!s) return GSG_OK;
   DeviceGuard dg(s->device);
-  cudaFree(s->nodes);
-  cudaFree(s->indptr);
-  cudaFree(s->indices);
+  gsg_ctx* c = s->owner;
+  if (c) {  // the big arrays go back to the context's spare list (reused by the next call)
+    auto& L = c->live_samples;
+    for (size_t i = 0; i < L.size(); i++)
+      if (L[i] == s) { L.erase(L.begin() + i); break; }
+    cudaDeviceSynchronize();  // as cudaFree would: no kernel may still read them when they are reused
+  }
+  pool_give(c, s->nodes, s->nodes_bytes);
+  pool_give(c, s->indptr, s->indptr_bytes);
+  pool_give(c, s->indices, s->indices_bytes);
   cudaFree(s->d_n);
   cudaFree(s->d_idx_off);
   cudaFree(s->d_err);
