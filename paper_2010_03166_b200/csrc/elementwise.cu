@@ -164,25 +164,56 @@ __global__ void __launch_bounds__(1024) k_head_final(int nblocks, int n, const f
 
 // dst row r = src row idx[r] (row_bytes each): 16-byte vectors when every address and pitch is
 // 16-byte aligned, bytes otherwise. One warp per row.
+// A warp copies RG rows at a time, every load of the group issued before its stores (rows are
+// random rows of a large source -- HBM latency -- and short: 800 B of features, 107 B of labels),
+// 16-byte words when every address and pitch allows, bytes otherwise; idx < 0 writes zeros.
+constexpr int RG = 4;
 __global__ void k_gather_rows(int rows, int64_t row_bytes, const uint8_t* __restrict__ src, int64_t sp,
                               const int32_t* __restrict__ idx, uint8_t* __restrict__ dst, int64_t dp, int vec) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
-    const int32_t j = __ldg(idx + r);
-    const uint8_t* s = src + (int64_t)j * sp;
-    uint8_t* d = dst + (int64_t)r * dp;
-    if (j < 0) {  // a padding row (gsg_sample_load): zeros
-      if (vec) {
-        for (int64_t k = lane; k < row_bytes / 16; k += 32) reinterpret_cast<uint4*>(d)[k] = make_uint4(0, 0, 0, 0);
-      } else {
-        for (int64_t k = lane; k < row_bytes; k += 32) d[k] = 0;
+  for (int r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RG; r0 < rows; r0 += warps * RG) {
+    int32_t j[RG];
+#pragma unroll
+    for (int g = 0; g < RG; g++) j[g] = r0 + g < rows ? __ldg(idx + r0 + g) : -2;  // -2: no such row
+    if (vec) {
+      const int64_t words = row_bytes / 16;
+      for (int64_t k0 = 0; k0 < words; k0 += 64) {
+        uint4 v[RG][2];
+#pragma unroll
+        for (int g = 0; g < RG; g++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int64_t k = k0 + lane + 32 * h;
+            v[g][h] = j[g] >= 0 && k < words ? __ldg(reinterpret_cast<const uint4*>(src + (int64_t)j[g] * sp) + k)
+                                             : make_uint4(0, 0, 0, 0);
+          }
+#pragma unroll
+        for (int g = 0; g < RG; g++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int64_t k = k0 + lane + 32 * h;
+            if (j[g] >= -1 && k < words) reinterpret_cast<uint4*>(dst + (int64_t)(r0 + g) * dp)[k] = v[g][h];
+          }
       }
-    } else if (vec) {
-      for (int64_t k = lane; k < row_bytes / 16; k += 32)
-        reinterpret_cast<uint4*>(d)[k] = __ldg(reinterpret_cast<const uint4*>(s) + k);
     } else {
-      for (int64_t k = lane; k < row_bytes; k += 32) d[k] = s[k];
+      for (int64_t k0 = 0; k0 < row_bytes; k0 += 128) {
+        uint8_t v[RG][4];
+#pragma unroll
+        for (int g = 0; g < RG; g++)
+#pragma unroll
+          for (int h = 0; h < 4; h++) {
+            const int64_t k = k0 + lane + 32 * h;
+            v[g][h] = j[g] >= 0 && k < row_bytes ? src[(int64_t)j[g] * sp + k] : (uint8_t)0;
+          }
+#pragma unroll
+        for (int g = 0; g < RG; g++)
+#pragma unroll
+          for (int h = 0; h < 4; h++) {
+            const int64_t k = k0 + lane + 32 * h;
+            if (j[g] >= -1 && k < row_bytes) dst[(int64_t)(r0 + g) * dp + k] = v[g][h];
+          }
+      }
     }
   }
 }
@@ -197,7 +228,7 @@ int gather_rows_launch(gsg_ctx* ctx, int rows, int64_t row_bytes, const void* sr
   GSG_CHECK(src_pitch >= row_bytes && dst_pitch >= row_bytes, GSG_EINVAL, "gather: pitch < row_bytes");
   const int vec = ((uintptr_t)src | (uintptr_t)dst | src_pitch | dst_pitch | row_bytes) % 16 == 0;
   ProfScope ps(ctx, GSG_K_OTHER, 2.0 * rows * row_bytes + 4.0 * rows, 0.0);
-  int grid = (int)(((int64_t)rows * 32 + 255) / 256);
+  int grid = (int)(((int64_t)(rows + RG - 1) / RG * 32 + 255) / 256);
   if (grid > ctx->num_sms * 16) grid = ctx->num_sms * 16;
   k_gather_rows<<<grid, 256, 0, ctx->stream>>>(rows, row_bytes, (const uint8_t*)src, src_pitch, idx, (uint8_t*)dst,
                                                dst_pitch, vec);

@@ -547,7 +547,14 @@ __global__ void k_sample_load(const int32_t* __restrict__ d_k, int n_cap, const 
     }
   }
   const int32_t* src = s_indices + s_off[k];
-  for (int64_t e = t0; e < nnz; e += T) indices[e] = src[e];
+  for (int64_t e0 = t0; e0 < nnz; e0 += 4 * T) {  // 4 loads in flight per thread
+    int32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) v[u] = e0 + u * T < nnz ? __ldg(src + e0 + u * T) : 0;
+#pragma unroll
+    for (int u = 0; u < 4; u++)
+      if (e0 + u * T < nnz) indices[e0 + u * T] = v[u];
+  }
 }
 
 __global__ void k_advance(int32_t* d_k, int count) { *d_k = (*d_k + 1) % count; }

@@ -143,3 +143,34 @@ def test_sample_load_overflow_is_reported(setup):
 
 def _ptr(t):
     return t.data_ptr()
+
+
+@pytest.mark.parametrize("dtype,cols,pitch", [(torch.float32, 200, 200), (torch.float32, 50, 56), (torch.uint8, 107, 107),
+                                              (torch.uint8, 1, 3), (torch.uint8, 33, 48), (torch.int32, 1, 1)])
+@pytest.mark.parametrize("rows", [1, 5, 1000])
+def test_gather_rows_exact(dtype, cols, pitch, rows):
+    """gsg_gather_rows == numpy fancy indexing, byte for byte (the 16-byte and the byte path, a
+    partial last group of rows, padding rows idx = -1 written as zeros, destination padding
+    columns untouched)."""
+    rng = np.random.default_rng(rows * 31 + cols)
+    n_src = 3000
+    if dtype == torch.uint8:
+        src_h = rng.integers(0, 256, (n_src, pitch), dtype=np.uint8)
+    elif dtype == torch.int32:
+        src_h = rng.integers(-2**31, 2**31 - 1, (n_src, pitch), dtype=np.int32)
+    else:
+        src_h = rng.standard_normal((n_src, pitch)).astype(np.float32)
+    idx_h = rng.integers(0, n_src, rows).astype(np.int32)
+    idx_h[rng.random(rows) < 0.1] = -1
+    src = torch.from_numpy(src_h).cuda()[:, :cols]
+    dst_full = torch.from_numpy(np.full((rows, pitch), 77, dtype=src_h.dtype)).cuda()
+    dst = dst_full[:, :cols]
+    idx = torch.from_numpy(idx_h).cuda()
+    ctx = gsg.Context(0)
+    ctx.gather_rows(src, idx.data_ptr(), dst, rows)
+    ctx.sync()
+    ref = np.where(idx_h[:, None] >= 0, src_h[np.maximum(idx_h, 0), :cols], 0).astype(src_h.dtype)
+    got = dst_full.cpu().numpy()
+    assert np.array_equal(got[:, :cols], ref)
+    assert np.all(got[:, cols:] == 77)
+    ctx.close()

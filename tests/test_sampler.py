@@ -336,3 +336,32 @@ def test_gpu_sample_assign_and_gather():
     with pytest.raises(gsg.GsgError):  # device arrays cannot be validated on the host
         info = batch.get(0)
         sg.assign(info["n"], info["nnz"], info["d_indptr"], info["d_indices"], validate=True)
+
+
+@pytest.mark.gpu
+def test_gpu_sample_batches_reuse_buffers():
+    """gsg_sample_free hands a batch's arrays back to its context and the next gsg_frontier_sample
+    reuses them (gsg.h): a reused batch must equal a batch drawn in a fresh context, including
+    a smaller second batch (fewer samples, different n) over the larger batch's stale contents; a
+    batch freed after its context was destroyed frees its own arrays."""
+    import paper_2010_03166_b200 as gsg
+    p = parent(n=6000, deg=12.0, seed=7)
+    ctx = gsg.Context(0)
+    pg = gsg.ParentGraph(ctx, p.indptr, p.indices)
+    first = pg.sample(900, 60, 11, count=5, clip=4)
+    first.free()  # its arrays go to the context's pool
+    second = pg.sample(700, 50, 22, count=3, clip=4)  # drawn into (some of) the reused arrays
+    fresh_ctx = gsg.Context(0)
+    fresh = gsg.ParentGraph(fresh_ctx, p.indptr, p.indices).sample(700, 50, 22, count=3, clip=4)
+    for k in range(3):
+        a, b = second.to_host(k), fresh.to_host(k)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b)), f"sample {k} differs after buffer reuse"
+        v = orc.frontier_sample(p.indptr, p.indices, 700, 50, 4, sampler_seed(22, k))
+        assert np.array_equal(a[2], v)
+    fresh.free()
+    fresh_ctx.close()
+    third = pg.sample(900, 60, 33, count=2, clip=4)
+    pg.free()
+    ctx.close()  # destroys the context while `third` is alive
+    third.free()  # frees its own arrays (no pool left)
+    second.free()
