@@ -69,12 +69,16 @@ enum {
   GSG_PREC_TF32 = 0,       /* fp32 operands read as TF32 by tcgen05 (kind::tf32), fp32 acc */
   GSG_PREC_BF16 = 1,       /* bf16 operand copies (kind::f16), fp32 accumulate             */
   GSG_PREC_FP32X3 = 2      /* fp32-accurate GEMM on TF32 tensor cores (3xTF32): each fp32
-                              operand x = hi + lo with hi = tf32_rn(x), lo = x - hi, and
-                              op(A) op(B) = Ahi Bhi + Ahi Blo + Alo Bhi (the lo x lo term,
-                              ~2^-22 relative, is dropped), evaluated as ONE TF32 GEMM over
-                              K' = 3K on split copies [Ahi | Ahi | Alo] and [Bhi ; Blo ; Bhi]
-                              made in the context workspace. ~1e-6 relative per product;
-                              3x the tensor work of TF32. fp32 operands like GSG_PREC_TF32. */
+                              operand x = hi + lo with hi = tf32_trunc(x) (kind::tf32 reads an
+                              fp32 operand truncated: the operand itself is hi), lo = x - hi,
+                              and op(A) op(B) = Ahi Bhi + Ahi Blo + Alo Bhi (the lo x lo term,
+                              ~2^-20 relative, is dropped), evaluated as ONE TF32 GEMM over
+                              K' = 3K whose k-block segments read [A | A | Alo] x [B ; Blo ; B];
+                              only Alo, Blo (and copies of operands TMA cannot read in place)
+                              are written, in the context workspace. ~1e-6 relative per
+                              product; 3x the tensor work of TF32. fp32 operands like
+                              GSG_PREC_TF32. (GSG_X3_IMPLICIT=0: the round-to-nearest split
+                              with three stacked copies, for comparison.) */
 };
 
 /* ---- flags --------------------------------------------------------------------------- */
@@ -230,7 +234,7 @@ GSG_API int gsg_spmm(gsg_ctx_t ctx, gsg_subgraph_t sg, int transpose, int32_t f,
  *          (lda >= M), i.e. op(A) = Aᵀ. Same for B: transB = 0 -> K x N (ldb >= N);
  *          transB = 1 -> stored N x K (ldb >= K).
  *   precision    GSG_PREC_TF32 / GSG_PREC_FP32X3: A, B are float*; GSG_PREC_BF16: A, B are
- *                bf16 (uint16). FP32X3 needs 3K < 2^31 and workspace for the split copies.
+ *                bf16 (uint16). FP32X3 needs workspace for the lo copies (and 3K < 2^31).
  *   d_C, ldc     fp32 output; d_Clp, ldclp optional bf16 copy (NULL = none)
  *   epilogue     GSG_EPI_*; d_aux/ldaux is the M x N gate for GSG_EPI_MASK
  *   d_auxbits, ldauxb  GSG_EPI_MASK only: the gate as a ReLU bitmask (overrides d_aux)

@@ -140,6 +140,7 @@ struct GemmArgs {
   uint32_t* cbits;        // GSG_EPI_RELU: also write the bitmask 1[C > 0] (splits == 1 only)
   int64_t ldcb;
   uint32_t idesc;
+  int x3nkb;        // FP32X3 with implicit hi: k-blocks per segment of K' = [A | A | A_lo] x [B ; B_lo ; B] (0: off)
 };
 
 // 1[x_i > 0] of one 32-column epilogue chunk (col0 % 32 == 0) as a bitmask word; columns past
@@ -266,7 +267,8 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
 template <int BN, bool BF16, bool A_MN, bool B_MN, bool CTA2>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const GemmArgs g) {
+           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
+           const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, const GemmArgs g) {
   using C = Cfg<BN, BF16, CTA2>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -289,6 +291,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (g.x3nkb) {
+      prefetch_tmap(&tmA2);
+      prefetch_tmap(&tmB2);
+    }
     if (g.tma_store) prefetch_tmap(&tmC);
     for (int s = 0; s < C::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; a++) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], CTA2 ? 2 * kEpiWarps : kEpiWarps); }
@@ -330,39 +336,51 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          const int k0 = kb * C::BK;
+          // FP32X3 (implicit hi): k-block kb of segment seg reads A (seg 0, 1) or A_lo (seg 2) and
+          // B (seg 0, 2) or B_lo (seg 1) at the segment's own k; each segment's last box is
+          // zero-filled by TMA past K
+          const CUtensorMap* pA = &tmA;
+          const CUtensorMap* pB = &tmB;
+          int kk = kb;
+          if (g.x3nkb) {
+            const int seg = kb / g.x3nkb;
+            kk = kb - seg * g.x3nkb;
+            if (seg == 2) pA = &tmA2;
+            if (seg == 1) pB = &tmB2;
+          }
+          const int k0 = kk * C::BK;
           if constexpr (CTA2) {
             const uint32_t lb = map_to_rank(smem_u32(&full[stage]), 0);
             if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
             if constexpr (A_MN) {
 #pragma unroll
               for (int j = 0; j < BM / C::MN_PER_ROW; j++)
-                tma_load_2d_pair(sa + j * (C::BK * 128), &tmA, lb, m0 + j * C::MN_PER_ROW, k0);
+                tma_load_2d_pair(sa + j * (C::BK * 128), pA, lb, m0 + j * C::MN_PER_ROW, k0);
             } else {
-              tma_load_2d_pair(sa, &tmA, lb, k0, m0);
+              tma_load_2d_pair(sa, pA, lb, k0, m0);
             }
             if constexpr (B_MN) {
 #pragma unroll
               for (int j = 0; j < C::BNC / C::MN_PER_ROW; j++)
-                tma_load_2d_pair(sb + j * (C::BK * 128), &tmB, lb, n0 + j * C::MN_PER_ROW, k0);
+                tma_load_2d_pair(sb + j * (C::BK * 128), pB, lb, n0 + j * C::MN_PER_ROW, k0);
             } else {
-              tma_load_2d_pair(sb, &tmB, lb, k0, n0);
+              tma_load_2d_pair(sb, pB, lb, k0, n0);
             }
           } else {
             mbar_expect_tx(&full[stage], C::STAGE_BYTES);
             if constexpr (A_MN) {
 #pragma unroll
               for (int j = 0; j < BM / C::MN_PER_ROW; j++)
-                tma_load_2d(sa + j * (C::BK * 128), &tmA, &full[stage], m0 + j * C::MN_PER_ROW, k0);
+                tma_load_2d(sa + j * (C::BK * 128), pA, &full[stage], m0 + j * C::MN_PER_ROW, k0);
             } else {
-              tma_load_2d(sa, &tmA, &full[stage], k0, m0);
+              tma_load_2d(sa, pA, &full[stage], k0, m0);
             }
             if constexpr (B_MN) {
 #pragma unroll
               for (int j = 0; j < C::BNC / C::MN_PER_ROW; j++)
-                tma_load_2d(sb + j * (C::BK * 128), &tmB, &full[stage], n0 + j * C::MN_PER_ROW, k0);
+                tma_load_2d(sb + j * (C::BK * 128), pB, &full[stage], n0 + j * C::MN_PER_ROW, k0);
             } else {
-              tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+              tma_load_2d(sb, pB, &full[stage], k0, n0);
             }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -768,6 +786,40 @@ __global__ void k_split3(int rows, int cols, const float* __restrict__ src, int6
   }
 }
 
+// FP32X3 with implicit hi: kind::tf32 reads an fp32 operand by truncating it to tf32 (measured:
+// 1 + 0.75 ulp_tf32 enters as 1), so the unmodified operand IS hi = trunc_tf32(x) to the tensor
+// core and only lo = x - trunc_tf32(x) (exact in fp32) is materialized, in the operand's own
+// stored shape. One warp per row, lanes along the row.
+// raw != nullptr: also copy x itself there (same ldd), for an operand whose stride or alignment
+// TMA cannot read directly.
+__global__ void k_split_lo(int rows, int cols, const float* __restrict__ src, int64_t lds, float* __restrict__ dst,
+                           int64_t ldd, float* __restrict__ raw) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+    const float* s = src + (int64_t)r * lds;
+    float* d = dst + (int64_t)r * ldd;
+    if ((cols & 3) == 0 && (lds & 3) == 0 && ((uintptr_t)src & 15) == 0) {  // ldd % 4 == 0, dst aligned
+      for (int c = lane; c < cols / 4; c += 32) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(s) + c);
+        float4 y;
+        y.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+        y.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+        y.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+        y.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+        reinterpret_cast<float4*>(d)[c] = y;
+        if (raw) reinterpret_cast<float4*>(raw + (int64_t)r * ldd)[c] = x;
+      }
+    } else {
+      for (int c = lane; c < cols; c += 32) {
+        const float x = __ldg(s + c);
+        d[c] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+        if (raw) raw[(int64_t)r * ldd + c] = x;
+      }
+    }
+  }
+}
+
 // --------------------------------------------------------------------------- host helpers
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -822,7 +874,7 @@ int make_store_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols,
 
 template <int BN, bool BF16, bool A_MN, bool B_MN, bool CTA2>
 int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const CUtensorMap& mx,
-             const GemmArgs& g) {
+             const CUtensorMap& ma2, const CUtensorMap& mb2, const GemmArgs& g) {
   using C = Cfg<BN, BF16, CTA2>;
   auto kern = k_gemm<BN, BF16, A_MN, B_MN, CTA2>;
   // function attributes are per device: set once for each device a context uses (racing
@@ -854,18 +906,19 @@ int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const C
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  GSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, g));
+  GSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, ma2, mb2, g));
   count_launch(ctx);
   return GSG_OK;
 }
 
 template <int BN, bool BF16, bool CTA2>
 int dispatch_major(gsg_ctx* ctx, bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
-                   const CUtensorMap& mc, const CUtensorMap& mx, const GemmArgs& g) {
-  if (!a_mn && !b_mn) return run_gemm<BN, BF16, false, false, CTA2>(ctx, ma, mb, mc, mx, g);
-  if (!a_mn && b_mn) return run_gemm<BN, BF16, false, true, CTA2>(ctx, ma, mb, mc, mx, g);
-  if (a_mn && !b_mn) return run_gemm<BN, BF16, true, false, CTA2>(ctx, ma, mb, mc, mx, g);
-  return run_gemm<BN, BF16, true, true, CTA2>(ctx, ma, mb, mc, mx, g);
+                   const CUtensorMap& mc, const CUtensorMap& mx, const CUtensorMap& ma2, const CUtensorMap& mb2,
+                   const GemmArgs& g) {
+  if (!a_mn && !b_mn) return run_gemm<BN, BF16, false, false, CTA2>(ctx, ma, mb, mc, mx, ma2, mb2, g);
+  if (!a_mn && b_mn) return run_gemm<BN, BF16, false, true, CTA2>(ctx, ma, mb, mc, mx, ma2, mb2, g);
+  if (a_mn && !b_mn) return run_gemm<BN, BF16, true, false, CTA2>(ctx, ma, mb, mc, mx, ma2, mb2, g);
+  return run_gemm<BN, BF16, true, true, CTA2>(ctx, ma, mb, mc, mx, ma2, mb2, g);
 }
 
 }  // namespace
@@ -874,7 +927,8 @@ namespace {
 int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA, const void* B,
                      int64_t ldb, int transB, float* Cp, int64_t ldc, void* Clp, int64_t ldclp, int precision,
                      int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate, const BitsIO& bits,
-                     bool x3);
+                     bool x3, const float* Alo = nullptr, int64_t ldalo = 0, const float* Blo = nullptr,
+                     int64_t ldblo = 0);
 }  // namespace
 
 int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
@@ -888,7 +942,7 @@ namespace {
 int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA, const void* B,
                      int64_t ldb, int transB, float* Cp, int64_t ldc, void* Clp, int64_t ldclp, int precision,
                      int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate, const BitsIO& bits,
-                     bool x3) {
+                     bool x3, const float* Alo, int64_t ldalo, const float* Blo, int64_t ldblo) {
   GSG_CHECK(precision == GSG_PREC_TF32 || precision == GSG_PREC_BF16 || precision == GSG_PREC_FP32X3, GSG_EINVAL,
             "bad precision %d", precision);
   GSG_CHECK(epilogue >= GSG_EPI_NONE && epilogue <= GSG_EPI_MASK, GSG_EINVAL, "bad epilogue %d", epilogue);
@@ -907,8 +961,37 @@ int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t l
             "bitmask gate needs GSG_EPI_MASK and ldauxb >= ceil(N/32) (ldauxb=%lld)", (long long)bits.ldi);
   GSG_CHECK(!bits.out || (epilogue == GSG_EPI_RELU && bits.ldo >= nwords && (uintptr_t)bits.out % 4 == 0), GSG_EINVAL,
             "bitmask output needs GSG_EPI_RELU and ldcb >= ceil(N/32) (ldcb=%lld)", (long long)bits.ldo);
+  static const int x3_implicit = getenv("GSG_X3_IMPLICIT") ? atoi(getenv("GSG_X3_IMPLICIT")) : 1;  // A/B
+  if (precision == GSG_PREC_FP32X3 && K > 0 && x3_implicit) {
+    // 3xTF32 with implicit hi: one TF32 GEMM over K' = 3K, segments [A | A | Alo] x [B ; Blo ; B]
+    // (the tensor core truncates the fp32 operand to hi itself); only Alo and Blo are written
+    GSG_CHECK(A && B, GSG_EINVAL, "A and B must be non-NULL");
+    const int64_t ar = transA ? K : M, ac = transA ? M : K, br = transB ? N : K, bc = transB ? K : N;
+    GSG_CHECK(lda >= ac && ldb >= bc, GSG_EINVAL, "lda / ldb below the stored widths");
+    const int64_t ldal = (ac + 3) / 4 * 4, ldbl = (bc + 3) / 4 * 4;
+    // an operand TMA cannot read in place (row pitch or base not 16-byte aligned) is copied too
+    const bool copy_a = lda % 4 != 0 || (uintptr_t)A % 16 != 0, copy_b = ldb % 4 != 0 || (uintptr_t)B % 16 != 0;
+    DevBuf* ws = ctx->side_ws ? ctx->ws_x3_side : ctx->ws_x3;
+    if (int rc = ws[0].reserve(sizeof(float) * ar * ldal * (copy_a ? 2 : 1))) return rc;
+    if (int rc = ws[1].reserve(sizeof(float) * br * ldbl * (copy_b ? 2 : 1))) return rc;
+    float* Al = static_cast<float*>(ws[0].ptr);
+    float* Bl = static_cast<float*>(ws[1].ptr);
+    float* Ar = copy_a ? Al + ar * ldal : nullptr;
+    float* Br = copy_b ? Bl + br * ldbl : nullptr;
+    auto grid_rows = [&](int64_t rows) {
+      return (int)std::min<int64_t>(std::max<int64_t>((rows * 32 + 255) / 256, 1), (int64_t)ctx->num_sms * 8);
+    };
+    k_split_lo<<<grid_rows(ar), 256, 0, ctx->stream>>>((int)ar, (int)ac, static_cast<const float*>(A), lda, Al, ldal, Ar);
+    k_split_lo<<<grid_rows(br), 256, 0, ctx->stream>>>((int)br, (int)bc, static_cast<const float*>(B), ldb, Bl, ldbl, Br);
+    count_launch(ctx, 2);
+    GSG_CUDA(cudaGetLastError());
+    return gemm_launch_impl(ctx, M, N, K, copy_a ? Ar : A, copy_a ? ldal : lda, transA, copy_b ? Br : B,
+                            copy_b ? ldbl : ldb, transB, Cp, ldc, Clp, ldclp, GSG_PREC_TF32, epilogue, aux, ldaux,
+                            split_k, accumulate, bits, true, Al, ldal, Bl, ldbl);
+  }
   if (precision == GSG_PREC_FP32X3 && K > 0) {
-    // 3xTF32: one TF32 GEMM over K' = 3K on split copies [Ahi | Ahi | Alo] x [Bhi ; Blo ; Bhi]
+    // 3xTF32 (GSG_X3_IMPLICIT=0): one TF32 GEMM over K' = 3K on split copies [Ahi | Ahi | Alo] x
+    // [Bhi ; Blo ; Bhi], hi rounded to nearest
     GSG_CHECK(A && B, GSG_EINVAL, "A and B must be non-NULL");
     GSG_CHECK(3LL * K < (int64_t)INT32_MAX, GSG_EUNSUPPORTED, "FP32X3 needs 3K < 2^31 (K=%d)", K);
     const int64_t K3 = 3LL * K;
@@ -939,8 +1022,9 @@ int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t l
   }
   if (precision == GSG_PREC_FP32X3) precision = GSG_PREC_TF32;  // K = 0: the epilogue of zero
   const bool bf16 = precision == GSG_PREC_BF16;
+  const double kx = Alo ? 3.0 : 1.0;  // implicit-hi FP32X3 executes K' = 3K
   ProfScope ps(ctx, GSG_K_GEMM,
-               (double)(bf16 ? 2 : 4) * ((double)M * K + (double)K * N) + 4.0 * M * N, 2.0 * M * N * K);
+               (double)(bf16 ? 2 : 4) * kx * ((double)M * K + (double)K * N) + 4.0 * M * N, 2.0 * M * N * K * kx);
   const int elem = bf16 ? 2 : 4;
   GemmArgs g{};
   g.M = M; g.N = N; g.K = K;
@@ -975,6 +1059,10 @@ int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t l
   g.num_m = (M + BMT - 1) / BMT;
   g.num_n = (N + BN - 1) / BN;
   g.num_kb = (K + BK - 1) / BK;
+  if (Alo) {  // K' = 3 segments of num_kb k-blocks each
+    g.x3nkb = g.num_kb;
+    g.num_kb *= 3;
+  }
   const int base_tiles = g.num_m * g.num_n;
   int splits = split_k;
   if (splits <= 0) {
@@ -1038,6 +1126,15 @@ int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t l
   if (transB) rc = make_map(&mb, B, bf16, N, K, ldb, BK, BNC, false);    // K-major B (stored N x K)
   else rc = make_map(&mb, B, bf16, K, N, ldb, mnrow, BK, true);          // MN-major B (stored K x N)
   if (rc) return rc;
+  CUtensorMap ma2 = ma, mb2 = mb;  // the lo operands of an implicit-hi FP32X3 GEMM (same boxes)
+  if (Alo) {
+    if (transA) rc = make_map(&ma2, Alo, false, K, M, ldalo, mnrow, BK, true);
+    else rc = make_map(&ma2, Alo, false, M, K, ldalo, BK, BM, false);
+    if (rc) return rc;
+    if (transB) rc = make_map(&mb2, Blo, false, N, K, ldblo, BK, BNC, false);
+    else rc = make_map(&mb2, Blo, false, K, N, ldblo, mnrow, BK, true);
+    if (rc) return rc;
+  }
   // epilogue store map: C itself, or the split-K workspace [splits * mpad x ldws]
   CUtensorMap mc;
   g.tma_store = accumulate ? 0 : 1;
@@ -1053,14 +1150,14 @@ int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t l
   }
   const bool a_mn = transA, b_mn = !transB;
   if (cta2) {
-    rc = bf16 ? dispatch_major<256, true, true>(ctx, a_mn, b_mn, ma, mb, mc, mx, g)
-              : dispatch_major<256, false, true>(ctx, a_mn, b_mn, ma, mb, mc, mx, g);
+    rc = bf16 ? dispatch_major<256, true, true>(ctx, a_mn, b_mn, ma, mb, mc, mx, ma2, mb2, g)
+              : dispatch_major<256, false, true>(ctx, a_mn, b_mn, ma, mb, mc, mx, ma2, mb2, g);
   } else if (bf16) {
-    rc = BN == 128 ? dispatch_major<128, true, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, g)
-                   : dispatch_major<256, true, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, g);
+    rc = BN == 128 ? dispatch_major<128, true, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, ma2, mb2, g)
+                   : dispatch_major<256, true, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, ma2, mb2, g);
   } else {
-    rc = BN == 128 ? dispatch_major<128, false, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, g)
-                   : dispatch_major<256, false, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, g);
+    rc = BN == 128 ? dispatch_major<128, false, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, ma2, mb2, g)
+                   : dispatch_major<256, false, false>(ctx, a_mn, b_mn, ma, mb, mc, mx, ma2, mb2, g);
   }
   if (rc) return rc;
   if (g.splits > 1) {

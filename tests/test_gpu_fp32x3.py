@@ -137,3 +137,35 @@ def test_gemm_fp32x3_long_k_auto_split(ctx, ta):
     rows = np.arange(0, M, 37)
     ref = orc.gemm(A[:, rows].T if ta else A[rows], B)
     assert rel_err(host(C)[rows], ref) <= X3_TOL
+
+
+def test_tf32_operand_is_truncated(ctx):
+    """The premise of FP32X3's implicit hi (gemm.cu k_split_lo): kind::tf32 reads an fp32 operand
+    by truncating it to tf32, so the unmodified operand is hi = trunc(x) and lo = x - trunc(x).
+    A single product 1 x (1 + 0.75 / 0.5 / 0.25 ulp_tf32) must come out as exactly 1 (rounding to
+    nearest would give 1 + ulp for 0.75); the negative case truncates toward zero."""
+    M = N = 128
+    K = 32
+    for v in (1 + 2**-11 + 2**-12, 1 + 2**-11, 1 + 2**-12, -(1 + 2**-11 + 2**-12)):
+        A = np.zeros((M, K), np.float32)
+        A[:, 0] = v
+        B = np.zeros((K, N), np.float32)
+        B[0, :] = 1.0
+        C = empty(M, N)
+        ctx.gemm(dev(A), dev(B), C, precision=gsg.GSG_PREC_TF32, K=K)
+        assert np.all(host(C) == np.float32(1.0 if v > 0 else -1.0)), (v, host(C)[0, 0])
+
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
+def test_gemm_fp32x3_unaligned_strides(ctx, ta, tb):
+    """FP32X3 takes operands whose row pitch TMA cannot read in place (ld % 4 != 0): the split
+    also copies them (implicit hi), same 1e-5."""
+    rng = np.random.default_rng(5)
+    M, N, K = 300, 130, 602
+    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    ref = orc.gemm(A, B, ta, tb)
+    C = empty(M, N)
+    ctx.gemm(dev(A, ld=A.shape[1] + 1), dev(B, ld=B.shape[1] + 2), C, transA=ta, transB=tb, precision=X3, K=K)
+    assert rel_err(host(C), ref) <= X3_TOL
