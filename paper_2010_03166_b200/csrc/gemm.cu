@@ -264,11 +264,13 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-template <int BN, bool BF16, bool A_MN, bool B_MN, bool CTA2>
-__global__ void __launch_bounds__(kGemmThreads, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
-           const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, const GemmArgs g) {
+// The kernel body; the tensor maps are references to the launching kernel's __grid_constant__
+// parameters (k_gemm: four maps; k_gemm_x3 adds the two lo operands of an implicit-hi FP32X3
+// GEMM, so that plain launches keep their parameter block as it was).
+template <int BN, bool BF16, bool A_MN, bool B_MN, bool CTA2, bool X3>
+__device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                                          const CUtensorMap& tmX, const CUtensorMap& tmA2, const CUtensorMap& tmB2,
+                                          const GemmArgs& g) {
   using C = Cfg<BN, BF16, CTA2>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
-    if (g.x3nkb) {
+    if constexpr (X3) {
       prefetch_tmap(&tmA2);
       prefetch_tmap(&tmB2);
     }
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const CUtensorMap* pA = &tmA;
           const CUtensorMap* pB = &tmB;
           int kk = kb;
-          if (g.x3nkb) {
+          if constexpr (X3) {
             const int seg = kb / g.x3nkb;
             kk = kb - seg * g.x3nkb;
             if (seg == 2) pA = &tmA2;
@@ -648,6 +650,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
+template <int BN, bool BF16, bool A_MN, bool B_MN, bool CTA2>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX, const GemmArgs g) {
+  gemm_body<BN, BF16, A_MN, B_MN, CTA2, false>(tmA, tmB, tmC, tmX, tmA, tmB, g);
+}
+
+template <int BN, bool BF16, bool A_MN, bool B_MN, bool CTA2>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm_x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
+              const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, const GemmArgs g) {
+  gemm_body<BN, BF16, A_MN, B_MN, CTA2, true>(tmA, tmB, tmC, tmX, tmA2, tmB2, g);
+}
+
 // Epilogue of one reduced float4 (columns c .. c+3 of row; w = valid columns).
 // With a ReLU bitmask output (FP32X3 splits only) the 4 columns' bits are OR-ed into their word,
 // which the GEMM's tile epilogue zeroed (OR commutes: the result does not depend on the order).
@@ -884,6 +901,11 @@ int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const C
   if (!(attr_devs.load(std::memory_order_acquire) & dbit)) {
     GSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     if (CTA2) GSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    if constexpr (!BF16) {
+      auto kern3 = k_gemm_x3<BN, false, A_MN, B_MN, CTA2>;
+      GSG_CUDA(cudaFuncSetAttribute(kern3, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+      if (CTA2) GSG_CUDA(cudaFuncSetAttribute(kern3, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    }
     attr_devs.fetch_or(dbit, std::memory_order_release);
   }
   const int tiles = g.num_m * g.num_n * g.splits;
@@ -906,7 +928,12 @@ int run_gemm(gsg_ctx* ctx, const CUtensorMap& ma, const CUtensorMap& mb, const C
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  GSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, ma2, mb2, g));
+  if constexpr (!BF16) {
+    if (g.x3nkb) GSG_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_x3<BN, false, A_MN, B_MN, CTA2>, ma, mb, mc, mx, ma2, mb2, g));
+    else GSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, g));
+  } else {
+    GSG_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, g));
+  }
   count_launch(ctx);
   return GSG_OK;
 }
