@@ -141,6 +141,7 @@ struct GemmArgs {
   int64_t ldcb;
   uint32_t idesc;
   int x3nkb;        // FP32X3 with implicit hi: k-blocks per segment of K' = [A | A | A_lo] x [B ; B_lo ; B] (0: off)
+  int x3dual;       // k_gemm_x3: each tile's K piece split over both TMEM accumulators (pieces > 32 k-blocks)
 };
 
 // 1[x_i > 0] of one 32-column epilogue chunk (col0 % 32 == 0) as a bitmask word; columns past
@@ -400,10 +401,22 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
         const int per_split = g.num_m * g.num_n;
         const int s = t / per_split;
         const int kb0 = s * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        // X3 (FP32X3): each tile's K piece in two halves, one per TMEM accumulator (each half
+        // <= 32 k-blocks: the accumulator drift bound), added by the epilogue in order -- two
+        // pieces per tile without a split-K reduction; both accumulators belong to every tile
+        const bool dual = X3 && g.x3dual;
+        const int half = dual ? (kb1 - kb0 + 1) / 2 : kb1 - kb0;
+        if (dual) {
+          mbar_wait(&tempty[0], acc_phase ^ 1);
+          mbar_wait(&tempty[1], acc_phase ^ 1);
+        } else {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+        }
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; kb++) {
+          const int ai = dual ? (kb - kb0 >= half ? 1 : 0) : acc;
+          const int kstart = dual && ai ? kb0 + half : kb0;
+          const uint32_t tmem_d = tmem_base + ai * BN;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * C::STAGE_BYTES);
@@ -415,7 +428,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             else ad = smem_desc<2>(a_addr + kk * 32, 16, 1024);
             if constexpr (B_MN) bd = mn_desc<BF16, C::BK>(b_addr, kk);
             else bd = smem_desc<2>(b_addr + kk * 32, 16, 1024);
-            const uint32_t en = (kb > kb0 || kk > 0) ? 1u : 0u;
+            const uint32_t en = (kb > kstart || kk > 0) ? 1u : 0u;
             if constexpr (CTA2) tc_mma_pair<BF16>(tmem_d, ad, bd, g.idesc, en);
             else tc_mma<BF16>(tmem_d, ad, bd, g.idesc, en);
           }
@@ -423,9 +436,10 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
           else tc_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        if constexpr (CTA2) tc_commit_pair(&tfull[acc]);
-        else tc_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if constexpr (CTA2) tc_commit_pair(&tfull[dual ? 0 : acc]);
+        else tc_commit(&tfull[dual ? 0 : acc]);
+        if (dual) acc_phase ^= 1;
+        else if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
   } else if (warp >= 4) {
@@ -444,8 +458,14 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
       const int per_split = g.num_m * g.num_n;
       const int s = t / per_split, r = t % per_split;
       const int mb = r / g.num_n, nb = r % g.num_n;
-      mbar_wait(&tfull[acc], acc_phase);
+      const bool dual = X3 && g.x3dual;
+      mbar_wait(&tfull[dual ? 0 : acc], acc_phase);
       tc_fence_after();
+      bool second = false;  // dual: the tile's second K half sits in accumulator 1
+      if (dual) {
+        const int kb0 = s * g.kb_per_split, kb1 = min(g.num_kb, kb0 + g.kb_per_split);
+        second = kb1 - kb0 > (kb1 - kb0 + 1) / 2;
+      }
       const int row_base = mb * C::BMT + (int)rank * BM + q * 32;
       const int row = row_base + lane;
       const bool row_ok = row < g.M;
@@ -453,7 +473,13 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
       for (int c = c_begin; c < c_begin + CPW; c++) {
         uint32_t v[32];
         __syncwarp();
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (dual ? 0 : acc) * BN + c * 32, v);
+        if (second) {
+          uint32_t v2[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + BN + c * 32, v2);
+#pragma unroll
+          for (int i = 0; i < 32; i++) v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(v2[i]));
+        }
         const int col0 = nb * BN + c * 32;
         if (g.tma_store) {
           if (row_base >= g.M || col0 >= g.N) continue;  // warp-uniform: block fully outside C
@@ -629,10 +655,21 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CTA2) mbar_arrive_cluster(tempty_leader + acc * 8);
-        else mbar_arrive(&tempty[acc]);
+        if (dual) {
+          if constexpr (CTA2) {
+            mbar_arrive_cluster(tempty_leader);
+            mbar_arrive_cluster(tempty_leader + 8);
+          } else {
+            mbar_arrive(&tempty[0]);
+            mbar_arrive(&tempty[1]);
+          }
+        } else {
+          if constexpr (CTA2) mbar_arrive_cluster(tempty_leader + acc * 8);
+          else mbar_arrive(&tempty[acc]);
+        }
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (dual) acc_phase ^= 1;
+      else if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (g.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
@@ -1124,11 +1161,16 @@ int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t l
   // (max-normalized 1.5e-5 at K' = 3600, 4.9e-5 at 12000, measured), past the 1e-5 the split
   // precision is for; the pieces are summed by the fixed-order reduction in fp32, which also
   // writes the ReLU bitmask then
-  if (split_k <= 0 && x3 && splits < (g.num_kb + 31) / 32) splits = (g.num_kb + 31) / 32;
+  // (the implicit-hi kernel accumulates each split in two TMEM halves: 64 k-blocks per split)
+  const int x3_cap = Alo ? 64 : 32;
+  if (split_k <= 0 && x3 && splits < (g.num_kb + x3_cap - 1) / x3_cap) splits = (g.num_kb + x3_cap - 1) / x3_cap;
   // TF32 / BF16: the bitmask is written by the tile epilogue, not the split-K reduction
   if (bits.out && !x3) splits = 1;
   if (splits > g.num_kb) splits = g.num_kb;
   g.kb_per_split = (g.num_kb + splits - 1) / splits;
+  // two TMEM halves per tile only where a piece is longer than the 32-k-block drift bound; shorter
+  // pieces keep the accumulator ping-pong (epilogue of one tile under the next tile's mainloop)
+  g.x3dual = Alo && g.kb_per_split > 32 ? 1 : 0;
   g.splits = (g.num_kb + g.kb_per_split - 1) / g.kb_per_split;  // no empty split
   g.mpad = g.num_m * BMT;
   if (g.splits > 1) {
