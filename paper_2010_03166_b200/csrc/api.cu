@@ -238,6 +238,7 @@ GSG_API int gsg_ctx_destroy(gsg_ctx_t c) {
   c->ws_lp0.release(); c->ws_lp1.release(); c->ws_lp2.release(); c->ws_loss.release();
   c->ws_mega.release(); c->ws_megactr.release(); c->ws_hseg.release(); c->ws_hsegctr.release();
   for (int i = 0; i < 2; i++) { c->ws_x3[i].release(); c->ws_x3_side[i].release(); }
+  c->ws_x3dz.release(); c->ws_x3hl.release();
   c->ws_sbits.release(); c->ws_svs.release(); c->ws_snv.release(); c->ws_swordpre.release(); c->ws_snnz.release();
   gsg::sampler_detach(c);  // live samples keep their arrays and free them themselves
   for (auto& b : c->spare) cudaFree(b.first);
@@ -647,12 +648,21 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
     const void* Wop2 = W;
     int64_t ldw2 = ldw;
     if (bf16 && (rc = bf16_weight(c, W, ldw, f_in, f_out, flags, &Wop2, &ldw2))) return rc;
+    X3Lo glo_b, glo_a;  // FP32X3: G's lo once for dW (B = G) and dX (A = G)
+    if (precision == GSG_PREC_FP32X3 && x3_implicit() && n > 0) {
+      const int64_t ldl = round_up(f_out, 4);
+      if ((rc = c->ws_x3dz.reserve(sizeof(float) * n * ldl))) return rc;
+      if ((rc = split_lo_launch(c, n, f_out, G, ldg, (float*)c->ws_x3dz.ptr, ldl))) return rc;
+      glo_b.b = glo_a.a = (const float*)c->ws_x3dz.ptr;
+      glo_b.ldb = glo_a.lda = ldl;
+    }
     rc = gemm_launch(c, f_in, f_out, n, bf16 ? Plp : (const void*)P, bf16 ? ldplp : ldp, 1, bf16 ? Glp : (const void*)G,
-                     ldg, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, (flags & GSG_ACCUM_DW) ? 1 : 0);
+                     ldg, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, (flags & GSG_ACCUM_DW) ? 1 : 0,
+                     BitsIO{}, glo_b);
     if (rc || !dX) return rc;
     c->prof_row = GSG_K_A6;
     return gemm_launch(c, n, f_in, f_out, bf16 ? Glp : (const void*)G, ldg, 0, Wop2, ldw2, 1, dX, lddx, dXlp, lddxlp,
-                       precision, gate ? GSG_EPI_MASK : GSG_EPI_NONE, Hbelow, ldhb, 0, 0, gb);
+                       precision, gate ? GSG_EPI_MASK : GSG_EPI_NONE, Hbelow, ldhb, 0, 0, gb, glo_a);
   }
   const void* Wop = W;
   int64_t ldwop = ldw;
@@ -664,12 +674,24 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   // capture), overlapping its fill / drain and split-K reduction with T's GEMM (config 5: -15 us
   // per step, configs 3-4 -0.2-0.7 %, config 2 +1 %). GSG_BWD_FORK=0 serializes them (A/B);
   // profiling serializes too (clean per-stage events).
+  // FP32X3: dZ's lo is split once for both GEMMs (it is B of dW and A of T, the same stored matrix)
+  X3Lo dzlo;
+  if (precision == GSG_PREC_FP32X3 && x3_implicit() && n > 0 && f_out > 0) {
+    const int64_t ldl = round_up(f_out, 4);
+    if ((rc = c->ws_x3dz.reserve(sizeof(float) * n * ldl))) return rc;
+    if ((rc = split_lo_launch(c, n, f_out, dZ, lddz, (float*)c->ws_x3dz.ptr, ldl))) return rc;
+    dzlo.a = dzlo.b = (const float*)c->ws_x3dz.ptr;
+    dzlo.lda = dzlo.ldb = ldl;
+  }
   SideFork fk(c, fork_enabled() && dX && !c->prof.on);
   // dW = Pᵀ dZ   (row a5): A = P stored n x f_in (MN-major), B = dZ stored n x f_out (MN-major)
   c->side_ws = true;
+  X3Lo dzlo_b;
+  dzlo_b.b = dzlo.b;
+  dzlo_b.ldb = dzlo.ldb;
   rc = gemm_launch(c, f_in, f_out, n, bf16 ? Plp : (const void*)P, bf16 ? ldplp : ldp, 1, bf16 ? dZlp : (const void*)dZ,
                    bf16 ? lddzlp : lddz, 0, dW, lddw, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0,
-                   (flags & GSG_ACCUM_DW) ? 1 : 0);
+                   (flags & GSG_ACCUM_DW) ? 1 : 0, BitsIO{}, dzlo_b);
   c->side_ws = false;
   fk.back();
   if (rc) return rc;
@@ -679,8 +701,11 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   const int64_t ldt = round_up(f_in, 4);
   if ((rc = c->ws_T.reserve(sizeof(float) * n * ldt))) return rc;
   float* T = (float*)c->ws_T.ptr;
+  X3Lo dzlo_a;
+  dzlo_a.a = dzlo.a;
+  dzlo_a.lda = dzlo.lda;
   rc = gemm_launch(c, n, f_in, f_out, bf16 ? dZlp : (const void*)dZ, bf16 ? lddzlp : lddz, 0, Wop, ldwop, 1, T, ldt,
-                   nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, 0);
+                   nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, 0, BitsIO{}, dzlo_a);
   if (rc) return rc;
   // dX = Âᵀ T [⊙ 1[H_below > 0]]   (row a7, fused a4 of the layer below)
   c->prof_row = GSG_K_A7;
@@ -768,14 +793,41 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
   const int hp = precision == GSG_PREC_FP32X3 ? GSG_PREC_FP32X3 : GSG_PREC_TF32;
   DeviceGuard dg(c->device);
   RowTag rt(c, GSG_K_A8);
-  int rc = gemm_launch(c, n, C, f, HL, ldh, 0, Wm, ldw, 0, S, lds, nullptr, 0, hp, GSG_EPI_NONE, nullptr, 0, 0, 0);
+  // FP32X3: H_L's lo serves S (A = H_L) and dW_mlp (A = H_Lᵀ, the same stored matrix), dS's lo
+  // dW_mlp (B) and dH_L (A): each split once
+  const bool x3pre = hp == GSG_PREC_FP32X3 && x3_implicit() && n > 0;
+  X3Lo hl_lo, ds_lo;
+  int rc;
+  if (x3pre) {
+    const int64_t ldl = round_up(f, 4);
+    if ((rc = c->ws_x3hl.reserve(sizeof(float) * n * ldl))) return rc;
+    if ((rc = split_lo_launch(c, n, f, HL, ldh, (float*)c->ws_x3hl.ptr, ldl))) return rc;
+    hl_lo.a = (const float*)c->ws_x3hl.ptr;
+    hl_lo.lda = ldl;
+  }
+  rc = gemm_launch(c, n, C, f, HL, ldh, 0, Wm, ldw, 0, S, lds, nullptr, 0, hp, GSG_EPI_NONE, nullptr, 0, 0, 0,
+                   BitsIO{}, hl_lo);
   if (rc) return rc;
   if ((rc = head_loss_launch(c, n, C, kind, S, lds, labels, node_w, dS, loss))) return rc;
+  if (x3pre) {
+    const int64_t ldl = round_up(C, 4);
+    if ((rc = c->ws_x3dz.reserve(sizeof(float) * n * ldl))) return rc;
+    if ((rc = split_lo_launch(c, n, C, dS, lds, (float*)c->ws_x3dz.ptr, ldl))) return rc;
+    ds_lo.a = ds_lo.b = (const float*)c->ws_x3dz.ptr;
+    ds_lo.lda = ds_lo.ldb = ldl;
+  }
+  X3Lo dwm_lo = hl_lo;  // dW_mlp = H_Lᵀ dS: A = H_L, B = dS
+  dwm_lo.b = ds_lo.b;
+  dwm_lo.ldb = ds_lo.ldb;
+  X3Lo dhl_lo;  // dH_L = dS W_mlpᵀ: A = dS
+  dhl_lo.a = ds_lo.a;
+  dhl_lo.lda = ds_lo.lda;
   // dW_mlp = H_Lᵀ dS and dH_L = (dS W_mlpᵀ) ⊙ 1[H_L > 0] only share read-only inputs: the first
   // runs on the side stream (fork / join, as in gsg_layer_backward; serialized while profiling)
   SideFork fk(c, fork_enabled() && !c->prof.on);
   c->side_ws = true;
-  rc = gemm_launch(c, f, C, n, HL, ldh, 1, dS, lds, 0, dWm, lddw, nullptr, 0, hp, GSG_EPI_NONE, nullptr, 0, 0, 0);
+  rc = gemm_launch(c, f, C, n, HL, ldh, 1, dS, lds, 0, dWm, lddw, nullptr, 0, hp, GSG_EPI_NONE, nullptr, 0, 0, 0,
+                   BitsIO{}, dwm_lo);
   c->side_ws = false;
   fk.back();
   if (rc) return rc;
@@ -783,7 +835,7 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
   gb.in = HLbits;
   gb.ldi = ldhlb;
   return gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, hp, GSG_EPI_MASK, HL, ldh,
-                     0, 0, gb);  // fk joins on exit
+                     0, 0, gb, dhl_lo);  // fk joins on exit
 }
 
 // ------------------------------------------------------------------------------ NCCL

@@ -115,6 +115,8 @@ struct gsg_ctx {
   gsg::DevBuf ws_loss;     // per-block loss partials
   gsg::DevBuf ws_x3[2];    // GSG_PREC_FP32X3 split operand copies (A3, B3), context stream
   gsg::DevBuf ws_x3_side[2];  // the same for the GEMMs that may be forked onto the side stream
+  gsg::DevBuf ws_x3dz;     // FP32X3: dZ's (dS's) lo, split once per layer backward (head) for both of its GEMMs
+  gsg::DevBuf ws_x3hl;     // FP32X3: H_L's lo, split once per head call for S and dW_mlp
   gsg::DevBuf ws_hseg;     // SpMM heavy-row segment partials
   gsg::DevBuf ws_hsegctr;  // SpMM heavy-row (row, chunk) arrival counters, zero between launches
   gsg::DevBuf ws_mega;     // SpMM mega-row segment partials
@@ -215,10 +217,21 @@ struct BitsIO {
 int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, const float* X, int64_t ldx,
                 float* Y, int64_t ldy, void* Ylp, int64_t ldylp, const float* mask, int64_t ldm, int relu = 0,
                 int accum = 0, const BitsIO& bits = BitsIO{});
+// FP32X3 lo operands the caller already computed (split_lo_launch of the same stored matrix),
+// e.g. dZ's, shared by the backward's T and dW GEMMs; nullptr = split inside the GEMM call.
+struct X3Lo {
+  const float* a = nullptr;
+  int64_t lda = 0;
+  const float* b = nullptr;
+  int64_t ldb = 0;
+};
 int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA,
                 const void* B, int64_t ldb, int transB, float* C, int64_t ldc, void* Clp, int64_t ldclp,
                 int precision, int epilogue, const float* aux, int64_t ldaux, int split_k, int accumulate,
-                const BitsIO& bits = BitsIO{});
+                const BitsIO& bits = BitsIO{}, const X3Lo& pre = X3Lo{});
+// lo = x - trunc_tf32(x) of a row-major fp32 matrix (FP32X3 operand split), ldd % 4 == 0
+int split_lo_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t lds, float* dst, int64_t ldd);
+bool x3_implicit();  // FP32X3 runs the implicit-hi path (GSG_X3_IMPLICIT, default 1)
 int to_bf16_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t lds, void* dst, int64_t ldd);
 int gather_rows_launch(gsg_ctx* ctx, int rows, int64_t row_bytes, const void* src, int64_t src_pitch,
                        const int32_t* idx, void* dst, int64_t dst_pitch);

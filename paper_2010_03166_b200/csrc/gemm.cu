@@ -854,15 +854,24 @@ __global__ void k_split_lo(int rows, int cols, const float* __restrict__ src, in
     const float* s = src + (int64_t)r * lds;
     float* d = dst + (int64_t)r * ldd;
     if ((cols & 3) == 0 && (lds & 3) == 0 && ((uintptr_t)src & 15) == 0) {  // ldd % 4 == 0, dst aligned
-      for (int c = lane; c < cols / 4; c += 32) {
-        const float4 x = __ldg(reinterpret_cast<const float4*>(s) + c);
-        float4 y;
-        y.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-        y.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-        y.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-        y.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-        reinterpret_cast<float4*>(d)[c] = y;
-        if (raw) reinterpret_cast<float4*>(raw + (int64_t)r * ldd)[c] = x;
+      const int n4 = cols / 4;
+      for (int c0 = lane; c0 < n4; c0 += 128) {  // 4 loads in flight per lane
+        float4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          x[u] = c0 + 32 * u < n4 ? __ldg(reinterpret_cast<const float4*>(s) + c0 + 32 * u) : make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int c = c0 + 32 * u;
+          if (c >= n4) break;
+          float4 y;
+          y.x = x[u].x - __uint_as_float(__float_as_uint(x[u].x) & 0xFFFFE000u);
+          y.y = x[u].y - __uint_as_float(__float_as_uint(x[u].y) & 0xFFFFE000u);
+          y.z = x[u].z - __uint_as_float(__float_as_uint(x[u].z) & 0xFFFFE000u);
+          y.w = x[u].w - __uint_as_float(__float_as_uint(x[u].w) & 0xFFFFE000u);
+          reinterpret_cast<float4*>(d)[c] = y;
+          if (raw) reinterpret_cast<float4*>(raw + (int64_t)r * ldd)[c] = x[u];
+        }
       }
     } else {
       for (int c = lane; c < cols; c += 32) {
@@ -997,9 +1006,30 @@ int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t l
 
 int gemm_launch(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int transA, const void* B, int64_t ldb,
                 int transB, float* Cp, int64_t ldc, void* Clp, int64_t ldclp, int precision, int epilogue,
-                const float* aux, int64_t ldaux, int split_k, int accumulate, const BitsIO& bits) {
+                const float* aux, int64_t ldaux, int split_k, int accumulate, const BitsIO& bits, const X3Lo& pre) {
+  const bool x3 = precision == GSG_PREC_FP32X3;  // precomputed lo operands mean nothing otherwise
   return gemm_launch_impl(ctx, M, N, K, A, lda, transA, B, ldb, transB, Cp, ldc, Clp, ldclp, precision, epilogue, aux,
-                          ldaux, split_k, accumulate, bits, false);
+                          ldaux, split_k, accumulate, bits, false, x3 ? pre.a : nullptr, pre.lda, x3 ? pre.b : nullptr,
+                          pre.ldb);
+}
+
+static int split_grid(gsg_ctx* ctx, int64_t rows) {
+  return (int)std::min<int64_t>(std::max<int64_t>((rows * 32 + 255) / 256, 1), (int64_t)ctx->num_sms * 8);
+}
+
+int split_lo_launch(gsg_ctx* ctx, int rows, int cols, const float* src, int64_t lds, float* dst, int64_t ldd) {
+  GSG_CHECK(rows >= 0 && cols >= 0 && lds >= cols && ldd >= cols && ldd % 4 == 0 && (uintptr_t)dst % 16 == 0,
+            GSG_EINVAL, "split_lo: bad shape");
+  if (rows == 0 || cols == 0) return GSG_OK;
+  k_split_lo<<<split_grid(ctx, rows), 256, 0, ctx->stream>>>(rows, cols, src, lds, dst, ldd, nullptr);
+  count_launch(ctx);
+  GSG_CUDA(cudaGetLastError());
+  return GSG_OK;
+}
+
+bool x3_implicit() {
+  static const int v = getenv("GSG_X3_IMPLICIT") ? atoi(getenv("GSG_X3_IMPLICIT")) : 1;  // A/B
+  return v != 0;
 }
 
 namespace {
@@ -1025,8 +1055,7 @@ int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t l
             "bitmask gate needs GSG_EPI_MASK and ldauxb >= ceil(N/32) (ldauxb=%lld)", (long long)bits.ldi);
   GSG_CHECK(!bits.out || (epilogue == GSG_EPI_RELU && bits.ldo >= nwords && (uintptr_t)bits.out % 4 == 0), GSG_EINVAL,
             "bitmask output needs GSG_EPI_RELU and ldcb >= ceil(N/32) (ldcb=%lld)", (long long)bits.ldo);
-  static const int x3_implicit = getenv("GSG_X3_IMPLICIT") ? atoi(getenv("GSG_X3_IMPLICIT")) : 1;  // A/B
-  if (precision == GSG_PREC_FP32X3 && K > 0 && x3_implicit) {
+  if (precision == GSG_PREC_FP32X3 && K > 0 && x3_implicit()) {
     // 3xTF32 with implicit hi: one TF32 GEMM over K' = 3K, segments [A | A | Alo] x [B ; Blo ; B]
     // (the tensor core truncates the fp32 operand to hi itself); only Alo and Blo are written
     GSG_CHECK(A && B, GSG_EINVAL, "A and B must be non-NULL");
@@ -1036,22 +1065,28 @@ int gemm_launch_impl(gsg_ctx* ctx, int M, int N, int K, const void* A, int64_t l
     // an operand TMA cannot read in place (row pitch or base not 16-byte aligned) is copied too
     const bool copy_a = lda % 4 != 0 || (uintptr_t)A % 16 != 0, copy_b = ldb % 4 != 0 || (uintptr_t)B % 16 != 0;
     DevBuf* ws = ctx->side_ws ? ctx->ws_x3_side : ctx->ws_x3;
-    if (int rc = ws[0].reserve(sizeof(float) * ar * ldal * (copy_a ? 2 : 1))) return rc;
-    if (int rc = ws[1].reserve(sizeof(float) * br * ldbl * (copy_b ? 2 : 1))) return rc;
+    if (!(Alo && !copy_a))
+      if (int rc = ws[0].reserve(sizeof(float) * ar * ldal * (copy_a ? 2 : 1))) return rc;
+    if (!(Blo && !copy_b))
+      if (int rc = ws[1].reserve(sizeof(float) * br * ldbl * (copy_b ? 2 : 1))) return rc;
     float* Al = static_cast<float*>(ws[0].ptr);
     float* Bl = static_cast<float*>(ws[1].ptr);
     float* Ar = copy_a ? Al + ar * ldal : nullptr;
     float* Br = copy_b ? Bl + br * ldbl : nullptr;
-    auto grid_rows = [&](int64_t rows) {
-      return (int)std::min<int64_t>(std::max<int64_t>((rows * 32 + 255) / 256, 1), (int64_t)ctx->num_sms * 8);
-    };
-    k_split_lo<<<grid_rows(ar), 256, 0, ctx->stream>>>((int)ar, (int)ac, static_cast<const float*>(A), lda, Al, ldal, Ar);
-    k_split_lo<<<grid_rows(br), 256, 0, ctx->stream>>>((int)br, (int)bc, static_cast<const float*>(B), ldb, Bl, ldbl, Br);
-    count_launch(ctx, 2);
+    // a lo the caller computed (Alo / Blo here, X3Lo) is used as is for an operand TMA reads in place
+    const bool pre_a = Alo && !copy_a, pre_b = Blo && !copy_b;
+    if (!pre_a)
+      k_split_lo<<<split_grid(ctx, ar), 256, 0, ctx->stream>>>((int)ar, (int)ac, static_cast<const float*>(A), lda, Al,
+                                                             ldal, Ar);
+    if (!pre_b)
+      k_split_lo<<<split_grid(ctx, br), 256, 0, ctx->stream>>>((int)br, (int)bc, static_cast<const float*>(B), ldb, Bl,
+                                                             ldbl, Br);
+    count_launch(ctx, (pre_a ? 0 : 1) + (pre_b ? 0 : 1));
     GSG_CUDA(cudaGetLastError());
     return gemm_launch_impl(ctx, M, N, K, copy_a ? Ar : A, copy_a ? ldal : lda, transA, copy_b ? Br : B,
                             copy_b ? ldbl : ldb, transB, Cp, ldc, Clp, ldclp, GSG_PREC_TF32, epilogue, aux, ldaux,
-                            split_k, accumulate, bits, true, Al, ldal, Bl, ldbl);
+                            split_k, accumulate, bits, true, pre_a ? Alo : Al, pre_a ? ldalo : ldal, pre_b ? Blo : Bl,
+                            pre_b ? ldblo : ldbl);
   }
   if (precision == GSG_PREC_FP32X3 && K > 0) {
     // 3xTF32 (GSG_X3_IMPLICIT=0): one TF32 GEMM over K' = 3K on split copies [Ahi | Ahi | Alo] x

@@ -69,8 +69,26 @@ def main():
     print(json.dumps({"config": cfg.cid, "kernels": len(last), "span_us": round(span, 1),
                       "busy_us": round(busy, 1), "idle_us": round(span - busy, 1),
                       "gaps_us": sorted(gaps, reverse=True)[:12]}, indent=1))
+    import re
+
+    def short(n):  # the kernel's own name out of the (static-prefixed) mangled symbol: <len>k_name
+        m = re.search(r"::(k_[A-Za-z0-9_]+)\s*[<(]", n)  # demangled
+        if m:
+            return m.group(1)
+        for m in re.finditer(r"(\d+)(k_[A-Za-z0-9_]+)", n):
+            digits, ident = m.group(1), m.group(2)
+            for i in range(len(digits)):  # the length prefix may follow other digits (a hash)
+                ln = int(digits[i:])
+                if 2 <= ln <= len(ident) and (ln == len(ident) or not ident[ln].islower()):
+                    return ident[:ln]
+        return n[:60]
+
+    per = {}
     for s, e, n in last:
-        print(f"{s - t0:9.1f} {e - s:8.1f}  {n[:90]}")
+        print(f"{s - t0:9.1f} {e - s:8.1f}  {short(n):24s} {n[:90]}")
+        k = short(n)
+        per[k] = per.get(k, 0.0) + (e - s)
+    print(json.dumps({"kernel_us_in_span": {k: round(v, 1) for k, v in sorted(per.items(), key=lambda x: -x[1])}}, indent=1))
 
 
 if __name__ == "__main__":
