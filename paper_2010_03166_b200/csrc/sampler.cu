@@ -328,7 +328,8 @@ __device__ __forceinline__ bool sbit(const uint32_t* sb, int32_t v) { return (sb
 // kIU such loads in flight per lane, and the next node's row range is fetched while the current
 // row is scanned (888 config-5 samples: 26.3 -> 21.5 ms). The same scheme in the fill pass (int4
 // loads with a warp scan of the hit counts, or 8 four-byte loads per lane in flight) was slower
-// there (94 / 66 vs 60 ms): its cost is the ranking of the hits in shared memory, not the loads.
+// there (94 / 66 vs 60 ms; with four ballots per 16-byte group instead of the scan 56 vs 52 ms):
+// its cost is the ranking of the hits in shared memory and their stores, not the loads.
 constexpr int kIU = 4;
 
 __device__ __forceinline__ unsigned hit_bits(const uint32_t* sb, int4 w, int64_t k, int64_t b, int64_t e) {
