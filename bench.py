@@ -889,7 +889,11 @@ def main():
     # ---- optional: the same step fed by the GPU sampler (a fresh subgraph every step) ----
     gpu_loop = None
     if args.sampler == "gpu" and args.batch == 1:
-        gpu_loop = run_gpu_sampled(args, cfg, ctx, runner, stream, dev, rank, max(nnz_raw))
+        # thousands of back-to-back steps: the clocks show whether the power cap engaged (compare
+        # with a pooled run of similar length, e.g. --steps 1000)
+        with ClockSampler(local) as clk_loop:
+            gpu_loop = run_gpu_sampled(args, cfg, ctx, runner, stream, dev, rank, max(nnz_raw))
+        gpu_loop["clocks"] = clk_loop.summary()
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
