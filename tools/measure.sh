@@ -18,6 +18,9 @@ python bench.py --impl reference > $O/ref.json 2>/dev/null
 python tools/gemm_bench.py > $O/gemm_bench.json 2>&1                   # ours vs cuBLAS, graph-replayed
 WIDTHS=200,300,512,602,1024 python tools/spmm_bench.py > $O/spmm_widths.jsonl 2>&1
 python tools/step_gaps.py > $O/timeline_c5.txt 2>&1
+for c in 2 3 4; do CFG=$c python tools/step_gaps.py > $O/timeline_c$c.txt 2>&1; done
+python bench.py --steps 1000 --warmup 20 --no-cpu --no-e2e > $O/c5_long1000.json 2>/dev/null      # sustained (power cap)
+python bench.py --sampler gpu --no-cpu --no-e2e --steps 20 > $O/c5_sampled_loop.json 2>/dev/null  # GPU-sampled loop
 # launch list of the bench step (shares, not absolutes: cold cache, serialized)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $O/ncu_launch.log 2>&1
