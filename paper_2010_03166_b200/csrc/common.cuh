@@ -18,7 +18,7 @@ constexpr int kMegaMinDeg = 2048;   // deg' >= this -> the row is split over kMe
 constexpr int kMegaSegs = 8;
 constexpr int kBins = 32;           // log2 degree buckets
 constexpr int kNMega = 3 * kBins + 6;  // counters[]: number of mega rows (the first ones in perm)
-constexpr int kHSeg = 256;          // heavy rows are cut into warp segments of <= kHSeg neighbors
+constexpr int kHSeg = 256;          // heavy rows are cut into warp segments of <= kHSeg neighbors (normalize: 160-256 by size)
 constexpr int kNHSeg = 3 * kBins + 7;  // counters[]: number of heavy-row segments (normalize)
 
 void set_error(const char* fmt, ...);

@@ -1,6 +1,9 @@
 // normalize.cu -- SURVEY §8(a) row a1: build Â (self loops, values), its transposed values
 // (device gather form of Alg. 4) and the degree bins used by the SpMMs.
 // Everything is stream-ordered; no host synchronization.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace gsg {
@@ -133,7 +136,8 @@ __global__ void k_transpose_vals(int n, const int32_t* __restrict__ rowptr, cons
 // with one global atomic per (block, bucket) on a zeroed cursor (the order within a bucket is
 // immaterial: every row is summed by one warp or CTA in CSR order).
 __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t* __restrict__ counters,
-                              int32_t* __restrict__ perm, int4* __restrict__ htask, int32_t* __restrict__ hcount) {
+                              int32_t* __restrict__ perm, int4* __restrict__ htask, int32_t* __restrict__ hcount,
+                              int hseg_len) {
   __shared__ int cnt[kBins], base[kBins], off[kBins];
   if (threadIdx.x == 0) {
     int acc = 0, heavy = 0, mega = 0;
@@ -163,7 +167,7 @@ __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t
         // the heavy row's warp segments for the SpMM: ceil(d / kHSeg) equal pieces, contiguous
         // in htask at a place reserved by one atomic (the order of rows in the list is
         // immaterial: each row's partial sums are combined in segment order)
-        const int sc = (d + kHSeg - 1) / kHSeg, len = (d + sc - 1) / sc;
+        const int sc = (d + hseg_len - 1) / hseg_len, len = (d + sc - 1) / sc;
         const int first = atomicAdd(&counters[kNHSeg], sc);
         hcount[first] = sc;
         for (int s2 = 0; s2 < sc; s2++) htask[first + s2] = make_int4(i, rb + s2 * len, min(rb + d, rb + (s2 + 1) * len), first);
@@ -176,6 +180,20 @@ __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t
     if (b >= 0) perm[base[b] + r] = i;
     __syncthreads();
   }
+}
+
+// Segment length of heavy rows: about the neighbors one warp of the SpMM's persistent grid gathers
+// per launch (nnz' / (SMs x 24 warps)), in [160, kHSeg], a multiple of 32. On a small subgraph the
+// few tasks per warp make the longest task set the kernel's length, so finer segments balance
+// it; on a large one they only add combine work (SpMM steps, GSG_HSEG_LEN=160 / 192 / 224 / 256:
+// config 3 0.542 / 0.556 / 0.565 / 0.575 ms, config 4 2.062 / 1.952 / 1.960 / 1.968, config 5
+// 2.887 / 2.898 / 2.887 / 2.888; profiles/r02_hseg_len_ab.txt). GSG_HSEG_LEN fixes it (A/B).
+int hseg_len(const gsg_ctx* ctx, int64_t nnz_hat) {
+  static const int env = getenv("GSG_HSEG_LEN") ? atoi(getenv("GSG_HSEG_LEN")) : 0;
+  if (env >= 32) return env;
+  const int64_t per_warp = nnz_hat / ((int64_t)ctx->num_sms * 24);
+  const int64_t v = (per_warp + 31) / 32 * 32;  // rounded up to whole 32-neighbor groups
+  return (int)std::min<int64_t>(kHSeg, std::max<int64_t>(160, v));
 }
 
 }  // namespace
@@ -200,8 +218,9 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
   }
   sg->nnz_hat = nh;
   sg->norm_mode = mode;
-  {  // heavy-row segments: sum over heavy rows of ceil(deg'/kHSeg) <= nnz'/kHSeg + nnz'/kHeavyMinDeg
-    const size_t cap = (size_t)(nh / kHSeg + nh / kHeavyMinDeg + 1);
+  const int hl = hseg_len(ctx, nh);
+  {  // heavy-row segments: sum over heavy rows of ceil(deg'/hl) <= nnz'/hl + nnz'/kHeavyMinDeg
+    const size_t cap = (size_t)(nh / hl + nh / kHeavyMinDeg + 1);
     if (cap > sg->cap_hseg) {
       cudaFree(sg->htask); cudaFree(sg->hcount);
       sg->htask = nullptr; sg->hcount = nullptr;
@@ -238,7 +257,7 @@ int normalize_launch(gsg_ctx* ctx, gsg_subgraph* sg, int mode) {
       k_transpose_vals<<<wgrid, T, 0, st>>>(n, sg->rowptr, sg->col, sg->val, sg->valT, sg->counters + 3 * kBins + 4);
       count_launch(ctx);
     }
-    k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm, sg->htask, sg->hcount);
+    k_bin_scatter<<<grid, T, 0, st>>>(n, sg->rowptr, sg->counters, sg->perm, sg->htask, sg->hcount, hl);
     count_launch(ctx);
   }
   GSG_CUDA(cudaGetLastError());
