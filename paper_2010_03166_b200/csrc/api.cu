@@ -236,7 +236,7 @@ GSG_API int gsg_ctx_destroy(gsg_ctx_t c) {
   cudaStreamSynchronize(c->stream);
   c->ws_splitk.release(); c->ws_splitk_side.release(); c->ws_T.release(); c->ws_dZ.release();
   c->ws_lp0.release(); c->ws_lp1.release(); c->ws_lp2.release(); c->ws_loss.release();
-  c->ws_mega.release(); c->ws_megactr.release(); c->ws_hseg.release(); c->ws_hsegctr.release();
+  c->ws_mega.release(); c->ws_megactr.release(); c->ws_taskctr.release(); c->ws_hseg.release(); c->ws_hsegctr.release();
   for (int i = 0; i < 2; i++) { c->ws_x3[i].release(); c->ws_x3_side[i].release(); }
   c->ws_x3dz.release(); c->ws_x3hl.release();
   c->ws_sbits.release(); c->ws_svs.release(); c->ws_snv.release(); c->ws_swordpre.release(); c->ws_snnz.release();

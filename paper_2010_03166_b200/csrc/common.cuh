@@ -121,6 +121,7 @@ struct gsg_ctx {
   gsg::DevBuf ws_hsegctr;  // SpMM heavy-row (row, chunk) arrival counters, zero between launches
   gsg::DevBuf ws_mega;     // SpMM mega-row segment partials
   gsg::DevBuf ws_megactr;  // SpMM mega-row (row, chunk) arrival counters, zero between launches
+  gsg::DevBuf ws_taskctr;  // SpMM dynamic warp-task counter + CTA exit counter, zero between launches
   cudaStream_t side = nullptr;       // fork/join side stream (layer backward: dW next to T -> dX)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // gsg_frontier_sample: scratch of a call (V_s bitmaps, insertion lists, sizes) and the device

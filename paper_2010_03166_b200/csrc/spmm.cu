@@ -72,6 +72,8 @@ struct SpmmArgs {
   const int32_t* __restrict__ n_hseg_ptr;
   float4* __restrict__ hseg_ws;        // [segment][f4] partial sums of multi-segment rows
   int* __restrict__ hseg_ctr;          // [first segment][chunk] arrival counters (zero between launches)
+  int* __restrict__ task_ctr;          // dyn: [0] warp tasks handed out past the first GW, [1] CTAs done (zero between launches)
+  int dyn;                             // 1: warp tasks past the first round are claimed from task_ctr
 };
 
 constexpr int kWarps = 8;
@@ -287,6 +289,25 @@ __device__ __forceinline__ float4 acc_part(const Acc& A, int q) {
   return make_float4(A.v[2 * q].x, A.v[2 * q].y, A.v[2 * q + 1].x, A.v[2 * q + 1].y);
 }
 
+// Dynamic warp tasks (a.dyn): the first GW tasks go to the warps in order, every later one to the
+// warp that claims it from task_ctr[0] (one atomic per task, issued at the start of the previous
+// task). Rows are visited longest first, so the claims end the launch with all warps finishing
+// together instead of the static round-robin's spread (which accumulates up to one longest task
+// per pass over the rows). A task's arithmetic does not depend on which warp runs it, so results
+// stay bitwise reproducible. The last CTA to finish zeroes the counters for the next launch.
+__device__ __forceinline__ void task_ctr_release(const SpmmArgs& a) {
+  if (!a.dyn) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.task_ctr + 1, 1) == (int)gridDim.x - 1) {
+      a.task_ctr[0] = 0;
+      a.task_ctr[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
 // Full-warp kernel (f > 64): chunk = up to 64 float4 (256 columns), lane owns c4 and c4 + 32.
 // MINB resident 8-warp CTAs per SM: 3 (80 registers per thread, a few spill bytes) keeps more
 // gathers in flight on large problems (config 5 2.973 -> 2.945 ms, config 3 0.619 -> 0.594 ms);
@@ -330,7 +351,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
     const int hs = *a.n_hseg_ptr;
     const int64_t per = (int64_t)hs + n_light;
     const int64_t L = per * a.nchunks;
-    for (int64_t t = gw; t < L; t += GW) {
+    for (int64_t t = gw; t < L;) {
+      int claim = 0;  // the next task, claimed now so the atomic's round trip hides behind this one
+      if (a.dyn && lane == 0) claim = atomicAdd(a.task_ctr, 1);
+      const int64_t t_next = a.dyn ? GW + __shfl_sync(0xffffffffu, claim, 0) : t + GW;
       const int chunk = (int)(t / per);
       const int r = (int)(t % per);
       const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
@@ -366,6 +390,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
           warp_row_sum<false>(a, st, b, e, 16u * min(c4, lim - 1), 16u * min(c4 + 32, lim - 1), lane, A);
       }
       const bool act0 = c4 < lim, act1 = c4b < lim;
+      t = t_next;
       if (cnt == 1) {
         if (act0) store_row(a, row, c4, acc_part(A, 0), &mw0);
         if (act1) store_row(a, row, c4b, acc_part(A, 1), W256 ? &mw0 : &mw1);
@@ -401,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
         if (lane == 0) a.hseg_ctr[(int64_t)first * a.nchunks + chunk] = 0;  // ready for the next launch
       }
     }
+    task_ctr_release(a);
     return;
   }
 
@@ -516,7 +542,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
 
   // ---- phase 2: light rows, one warp per (row, chunk) ----
   const int64_t L = (int64_t)n_light * a.nchunks;
-  for (int64_t t = gw; t < L; t += GW) {
+  for (int64_t t = gw; t < L;) {
+    int claim = 0;
+    if (a.dyn && lane == 0) claim = atomicAdd(a.task_ctr, 1);
+    const int64_t t_next = a.dyn ? GW + __shfl_sync(0xffffffffu, claim, 0) : t + GW;
     const int chunk = (int)(t / n_light);
     const int row = a.perm[n_heavy + (int)(t % n_light)];
     const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
@@ -546,7 +575,9 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
     }
     if (c4 < lim) store_row(a, row, c4, acc_part(A, 0), &mw0);
     if (c4b < lim) store_row(a, row, c4b, acc_part(A, 1), W256 ? &mw0 : &mw1);
+    t = t_next;
   }
+  task_ctr_release(a);
 }
 
 // Sub-warp kernel (f <= 64): groups of G lanes, one row per group; heavy rows CTA-split.
@@ -728,6 +759,14 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
       a.n_hseg_ptr = sg->counters + kNHSeg;
       a.hseg_ws = static_cast<float4*>(ctx->ws_hseg.ptr);
       a.hseg_ctr = static_cast<int*>(ctx->ws_hsegctr.ptr);
+    }
+    static const int dyn_env = getenv("GSG_SPMM_DYN") ? atoi(getenv("GSG_SPMM_DYN")) : 1;  // A/B: 0 static
+    a.dyn = dyn_env ? 1 : 0;
+    if (a.dyn) {
+      const size_t had = ctx->ws_taskctr.bytes;
+      if (int rc = ctx->ws_taskctr.reserve(2 * sizeof(int))) return rc;
+      if (ctx->ws_taskctr.bytes != had) GSG_CUDA(cudaMemsetAsync(ctx->ws_taskctr.ptr, 0, ctx->ws_taskctr.bytes, ctx->stream));
+      a.task_ctr = static_cast<int*>(ctx->ws_taskctr.ptr);
     }
     a.cw = (a.f4 + a.nchunks - 1) / a.nchunks;
     static const int w256_env = getenv("GSG_SPMM_W256") ? atoi(getenv("GSG_SPMM_W256")) : 1;
