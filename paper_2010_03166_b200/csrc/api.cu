@@ -183,6 +183,18 @@ bool fork_enabled() {
   return f;
 }
 
+// GSG_BWD_TFIRST (A/B): 0 dW first (default), 1 T first in every layer, 2 T first where the
+// layer's input is narrower than its output (layer 1); GSG_HEAD_DHFIRST=1: the head's dH_L
+// before its forked dW_mlp
+bool t_first(int f_in, int f_out) {
+  static const int m = getenv("GSG_BWD_TFIRST") ? atoi(getenv("GSG_BWD_TFIRST")) : 0;
+  return m == 1 || (m == 2 && f_in < f_out);
+}
+bool head_dh_first() {
+  static const bool f = getenv("GSG_HEAD_DHFIRST") && atoi(getenv("GSG_HEAD_DHFIRST")) == 1;
+  return f;
+}
+
 // The bf16 weight operand of a layer GEMM: the caller's own copy (GSG_W_BF16: W is bf16 with
 // ldw in bf16 elements) or a conversion into the context workspace.
 int bf16_weight(gsg_ctx* c, const float* W, int64_t ldw, int f_in, int f_out, int flags, const void** out,
@@ -684,6 +696,29 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
     dzlo.lda = dzlo.ldb = ldl;
   }
   SideFork fk(c, fork_enabled() && dX && !c->prof.on);
+  const int64_t ldt = round_up(f_in, 4);
+  float* T = nullptr;
+  X3Lo dzlo_a;
+  dzlo_a.a = dzlo.a;
+  dzlo_a.lda = dzlo.lda;
+  // T = dZ Wᵀ   (row a6): A = dZ (K-major), B = W stored f_in x f_out = N x K (K-major)
+  auto launch_T = [&]() -> int {
+    c->prof_row = GSG_K_A6;
+    if (int r = c->ws_T.reserve(sizeof(float) * n * ldt)) return r;
+    T = (float*)c->ws_T.ptr;
+    return gemm_launch(c, n, f_in, f_out, bf16 ? dZlp : (const void*)dZ, bf16 ? lddzlp : lddz, 0, Wop, ldwop, 1, T,
+                       ldt, nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, 0, BitsIO{}, dzlo_a);
+  };
+  // GSG_BWD_TFIRST (A/B): T is enqueued on the main stream before the forked dW (both wait only
+  // for dZ), so T's CTAs take the SMs first and dW fills them as T's tiles run out
+  const bool tfirst = fk.away && t_first(f_in, f_out);
+  if (tfirst) {
+    c->stream = fk.main;
+    rc = launch_T();
+    c->stream = c->side;
+    if (rc) return rc;
+  }
+  c->prof_row = GSG_K_A5;
   // dW = Pᵀ dZ   (row a5): A = P stored n x f_in (MN-major), B = dZ stored n x f_out (MN-major)
   c->side_ws = true;
   X3Lo dzlo_b;
@@ -696,17 +731,7 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
   fk.back();
   if (rc) return rc;
   if (!dX) return GSG_OK;
-  c->prof_row = GSG_K_A6;
-  // T = dZ Wᵀ   (row a6): A = dZ (K-major), B = W stored f_in x f_out = N x K (K-major)
-  const int64_t ldt = round_up(f_in, 4);
-  if ((rc = c->ws_T.reserve(sizeof(float) * n * ldt))) return rc;
-  float* T = (float*)c->ws_T.ptr;
-  X3Lo dzlo_a;
-  dzlo_a.a = dzlo.a;
-  dzlo_a.lda = dzlo.lda;
-  rc = gemm_launch(c, n, f_in, f_out, bf16 ? dZlp : (const void*)dZ, bf16 ? lddzlp : lddz, 0, Wop, ldwop, 1, T, ldt,
-                   nullptr, 0, precision, GSG_EPI_NONE, nullptr, 0, 0, 0, BitsIO{}, dzlo_a);
-  if (rc) return rc;
+  if (!tfirst && (rc = launch_T())) return rc;
   // dX = Âᵀ T [⊙ 1[H_below > 0]]   (row a7, fused a4 of the layer below)
   c->prof_row = GSG_K_A7;
   return spmm_launch(c, sg, 1, f_in, T, ldt, dX, lddx, dXlp, lddxlp, Hbelow, ldhb, 0, 0, gb);  // fk joins on exit
@@ -825,17 +850,27 @@ GSG_API int gsg_head(gsg_ctx_t c, int32_t n, int32_t f, int32_t C, int kind, con
   // dW_mlp = H_Lᵀ dS and dH_L = (dS W_mlpᵀ) ⊙ 1[H_L > 0] only share read-only inputs: the first
   // runs on the side stream (fork / join, as in gsg_layer_backward; serialized while profiling)
   SideFork fk(c, fork_enabled() && !c->prof.on);
+  BitsIO gb;  // ReLU' gate of H_L: its bitmask when given
+  gb.in = HLbits;
+  gb.ldi = ldhlb;
+  auto launch_dHL = [&]() {
+    return gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, hp, GSG_EPI_MASK, HL, ldh, 0, 0,
+                       gb, dhl_lo);
+  };
+  const bool dh_first = fk.away && head_dh_first();
+  if (dh_first) {  // GSG_HEAD_DHFIRST (A/B): dH_L enqueued on the main stream before the forked dW_mlp
+    c->stream = fk.main;
+    rc = launch_dHL();
+    c->stream = c->side;
+    if (rc) return rc;
+  }
   c->side_ws = true;
   rc = gemm_launch(c, f, C, n, HL, ldh, 1, dS, lds, 0, dWm, lddw, nullptr, 0, hp, GSG_EPI_NONE, nullptr, 0, 0, 0,
                    BitsIO{}, dwm_lo);
   c->side_ws = false;
   fk.back();
   if (rc) return rc;
-  BitsIO gb;  // ReLU' gate of H_L: its bitmask when given
-  gb.in = HLbits;
-  gb.ldi = ldhlb;
-  return gemm_launch(c, n, f, C, dS, lds, 0, Wm, ldw, 1, dHL, lddh, dHlp, lddhlp, hp, GSG_EPI_MASK, HL, ldh,
-                     0, 0, gb, dhl_lo);  // fk joins on exit
+  return dh_first ? GSG_OK : launch_dHL();  // fk joins on exit
 }
 
 // ------------------------------------------------------------------------------ NCCL

@@ -295,6 +295,18 @@ __device__ __forceinline__ float4 acc_part(const Acc& A, int q) {
 // together instead of the static round-robin's spread (which accumulates up to one longest task
 // per pass over the rows). A task's arithmetic does not depend on which warp runs it, so results
 // stay bitwise reproducible. The last CTA to finish zeroes the counters for the next launch.
+// a.dyn == 2 (A/B): the first task is claimed too, so a CTA that becomes resident late (its SM
+// held by a concurrent kernel) does not start one of the longest tasks late
+__device__ __forceinline__ int64_t first_task(const SpmmArgs& a, int64_t gw, int lane) {
+  if (a.dyn != 2) return gw;
+  int c = 0;
+  if (lane == 0) c = atomicAdd(a.task_ctr, 1);
+  return __shfl_sync(0xffffffffu, c, 0);
+}
+__device__ __forceinline__ int64_t next_task(const SpmmArgs& a, int64_t t, int64_t GW, int claim) {
+  return a.dyn == 2 ? (int64_t)claim : (a.dyn ? GW + claim : t + GW);
+}
+
 __device__ __forceinline__ void task_ctr_release(const SpmmArgs& a) {
   if (!a.dyn) return;
   __syncthreads();
@@ -351,10 +363,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
     const int hs = *a.n_hseg_ptr;
     const int64_t per = (int64_t)hs + n_light;
     const int64_t L = per * a.nchunks;
-    for (int64_t t = gw; t < L;) {
+    for (int64_t t = first_task(a, gw, lane); t < L;) {
       int claim = 0;  // the next task, claimed now so the atomic's round trip hides behind this one
       if (a.dyn && lane == 0) claim = atomicAdd(a.task_ctr, 1);
-      const int64_t t_next = a.dyn ? GW + __shfl_sync(0xffffffffu, claim, 0) : t + GW;
+      const int64_t t_next = next_task(a, t, GW, __shfl_sync(0xffffffffu, claim, 0));
       const int chunk = (int)(t / per);
       const int r = (int)(t % per);
       const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
@@ -542,10 +554,10 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
 
   // ---- phase 2: light rows, one warp per (row, chunk) ----
   const int64_t L = (int64_t)n_light * a.nchunks;
-  for (int64_t t = gw; t < L;) {
+  for (int64_t t = first_task(a, gw, lane); t < L;) {
     int claim = 0;
     if (a.dyn && lane == 0) claim = atomicAdd(a.task_ctr, 1);
-    const int64_t t_next = a.dyn ? GW + __shfl_sync(0xffffffffu, claim, 0) : t + GW;
+    const int64_t t_next = next_task(a, t, GW, __shfl_sync(0xffffffffu, claim, 0));
     const int chunk = (int)(t / n_light);
     const int row = a.perm[n_heavy + (int)(t % n_light)];
     const int c0 = chunk * a.cw, lim = min(a.f4, c0 + a.cw);
@@ -761,7 +773,7 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
       a.hseg_ctr = static_cast<int*>(ctx->ws_hsegctr.ptr);
     }
     static const int dyn_env = getenv("GSG_SPMM_DYN") ? atoi(getenv("GSG_SPMM_DYN")) : 1;  // A/B: 0 static
-    a.dyn = dyn_env ? 1 : 0;
+    a.dyn = dyn_env == 2 ? 2 : (dyn_env ? 1 : 0);
     if (a.dyn) {
       const size_t had = ctx->ws_taskctr.bytes;
       if (int rc = ctx->ws_taskctr.reserve(2 * sizeof(int))) return rc;
