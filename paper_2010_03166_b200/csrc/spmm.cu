@@ -29,6 +29,7 @@
 #include <cstdlib>
 
 #include <atomic>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -74,6 +75,8 @@ struct SpmmArgs {
   int* __restrict__ hseg_ctr;          // [first segment][chunk] arrival counters (zero between launches)
   int* __restrict__ task_ctr;          // dyn: [0] warp tasks handed out past the first GW, [1] CTAs done (zero between launches)
   int dyn;                             // 1: warp tasks past the first round are claimed from task_ctr
+  int tailg;                           // > 0: the last column chunk (<= 2*tailg float4) is gathered by
+                                       // lane groups of tailg, 32/tailg neighbors per warp instruction
 };
 
 constexpr int kWarps = 8;
@@ -205,6 +208,72 @@ __device__ __forceinline__ void warp_row_sum256(const SpmmArgs& a, int2* __restr
     }
     __syncwarp();
   }
+}
+
+// The last, narrow column chunk of a row (r <= 2G float4, e.g. f = 300: 64 + 11 float4) with lane
+// groups of G: group g gathers neighbors g, g + 32/G, ... of the staged 32, so one warp-wide 256-bit
+// load instruction moves 32/G neighbor rows instead of one row with 32 - r/2 idle lanes (f = 300:
+// 1.25 instead of 2 load instructions per neighbor). Batches of 8 / 4 / 2 / 1 instructions cover
+// only the staged neighbors. The group sums are combined in a fixed tree (g0 + g1) + (g2 + g3) into
+// lanes 0..G-1 (every other lane's columns lie past the chunk and are never stored): deterministic.
+template <int G>
+__device__ __forceinline__ void warp_row_sum256_grp(const SpmmArgs& a, int2* __restrict__ st, int b, int e, uint32_t lo,
+                                                    int lane, Acc& A) {
+  constexpr int NG = 32 / G;
+  const int g = lane / G;
+  const char* X0 = reinterpret_cast<const char*>(a.X) + lo;
+#pragma unroll
+  for (int q = 0; q < 2 * V; q++) A.v[q] = make_float2(0.f, 0.f);
+  auto batch = [&](auto ub, int i) {
+    constexpr int UB = decltype(ub)::value;
+    int2 p[UB];
+#pragma unroll
+    for (int u = 0; u < UB; u++) p[u] = st[(i + u) * NG + g];
+    float4 x[UB][V];
+#pragma unroll
+    for (int u = 0; u < UB; u++) ld256(X0 + (uint32_t)p[u].x, x[u]);
+#pragma unroll
+    for (int u = 0; u < UB; u++) acc_fma(A, __int_as_float(p[u].y), x[u]);
+  };
+  for (int k0 = b; k0 < e; k0 += 32) {
+    const int k = k0 + lane;
+    int2 pr = make_int2(0, 0);
+    if (k < e) pr = make_int2((int)((uint32_t)__ldg(a.col + k) * a.ldx16), __float_as_int(__ldg(a.val + k)));
+    const int off0 = __shfl_sync(0xffffffffu, pr.x, 0);
+    if (k >= e) pr = make_int2(off0, 0);  // padding slots: the first neighbor's row again, weight 0
+    st[lane] = pr;
+    __syncwarp();
+    const int ni = (min(32, e - k0) + NG - 1) / NG;  // warp instructions for the staged neighbors
+    int i = 0;
+    for (; i + 8 <= ni; i += 8) batch(std::integral_constant<int, 8>{}, i);
+    if (i + 4 <= ni) { batch(std::integral_constant<int, 4>{}, i); i += 4; }
+    if (i + 2 <= ni) { batch(std::integral_constant<int, 2>{}, i); i += 2; }
+    if (i < ni) batch(std::integral_constant<int, 1>{}, i);
+    __syncwarp();
+  }
+#pragma unroll
+  for (int sh = G; sh < 32; sh <<= 1) {
+#pragma unroll
+    for (int q = 0; q < 2 * V; q++) {
+      A.v[q].x += __shfl_down_sync(0xffffffffu, A.v[q].x, sh);
+      A.v[q].y += __shfl_down_sync(0xffffffffu, A.v[q].y, sh);
+    }
+  }
+}
+
+// W256 gather of one (row range, chunk) task: the grouped tail path for the last chunk when
+// a.tailg is set, else one row per warp instruction
+template <int UU>
+__device__ __forceinline__ void gather256(const SpmmArgs& a, int2* __restrict__ st, int b, int e, int chunk, int c0,
+                                          int lim, int lane, Acc& A) {
+  if (a.tailg && chunk == a.nchunks - 1) {
+    const int G = a.tailg;
+    const uint32_t lo = 16u * (c0 + min(2 * (lane & (G - 1)), (lim - c0 - 1) & ~1));
+    if (G == 8) warp_row_sum256_grp<8>(a, st, b, e, lo, lane, A);
+    else warp_row_sum256_grp<16>(a, st, b, e, lo, lane, A);
+    return;
+  }
+  warp_row_sum256<UU>(a, st, b, e, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
 }
 
 // Sub-warp (group of G lanes, one row) accumulation; no shuffles (groups diverge).
@@ -392,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
       if (W256) {
         c4 = c0 + 2 * lane;
         c4b = c4 + 1;
-        warp_row_sum256<UU>(a, st, b, e, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
+        gather256<UU>(a, st, b, e, chunk, c0, lim, lane, A);
       } else {
         c4 = c0 + lane;
         c4b = c4 + 32;
@@ -484,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
     if (W256) {
       c4 = c0 + 2 * lane;
       c4b = c4 + 1;
-      warp_row_sum256<UU>(a, st, w0, w1, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
+      gather256<UU>(a, st, w0, w1, chunk, c0, lim, lane, A);
     } else {
       c4 = c0 + lane;
       c4b = c4 + 32;
@@ -576,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_spmm_wide(SpmmArgs a) {
     if (W256) {
       c4 = c0 + 2 * lane;
       c4b = c4 + 1;
-      warp_row_sum256<UU>(a, st, b, e, 16u * (c0 + min(2 * lane, (lim - c0 - 1) & ~1)), lane, A);
+      gather256<UU>(a, st, b, e, chunk, c0, lim, lane, A);
     } else {
       c4 = c0 + lane;
       c4b = c4 + 32;
@@ -784,6 +853,19 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
     static const int w256_env = getenv("GSG_SPMM_W256") ? atoi(getenv("GSG_SPMM_W256")) : 1;
     a.w256 = w256_env && (uintptr_t)X % 32 == 0 && ldx % 8 == 0;  // GSG_SPMM_W256=0: 128-bit path (A/B)
     if (a.w256) a.cw = (a.cw + 1) & ~1;  // chunks start on 32-byte column pairs
+    // a narrow remainder (r = f4 mod 64 <= 32 float4 past whole 64-float4 chunks) as its own chunk
+    // gathered by lane groups (warp_row_sum256_grp) instead of equal chunks with idle lanes:
+    // f = 300 -> 64 + 11 float4 (1.25 load instructions per neighbor instead of 2), f = 602 ->
+    // 64 + 64 + 23 (2.5 instead of 3). GSG_SPMM_TAIL=0 keeps equal chunks (A/B).
+    static const int tail_env = getenv("GSG_SPMM_TAIL") ? atoi(getenv("GSG_SPMM_TAIL")) : 1;
+    a.tailg = 0;
+    {
+      const int r = a.f4 % (32 * V);
+      if (tail_env && a.w256 && a.f4 > 32 * V && r > 0 && r <= 32) {
+        a.cw = 32 * V;
+        a.tailg = r <= 16 ? 8 : 16;
+      }
+    }
     const int64_t tasks = (int64_t)sg->n * a.nchunks;
     static const int minb_env = getenv("GSG_SPMM_MINB") ? atoi(getenv("GSG_SPMM_MINB")) : 0;  // A/B: force 2 or 3
     // three CTAs per SM from ~4 (row, chunk) tasks per warp on: config 5 / 4 f = 200 (20000 / 16000

@@ -173,6 +173,36 @@ def test_spmm_dense_frontier(ctx, f):
     assert torch.equal(Y, Y2)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("f", [260, 300, 320, 324, 384, 602, 1100])
+def test_spmm_lane_group_tail(ctx, f):
+    """The last column chunk gathered by lane groups (f4 mod 64 in [1, 32], 32-byte rows): group
+    sizes 8 (r <= 16 float4: f = 260, 300, 320) and 16 (f = 324, 384, 602, 1100), at the group-size
+    boundaries r = 1 / 16 / 17 / 32, on light rows, a CTA-split heavy row (degree 1,200 < the
+    mega-row bound, f >= 1024 launches) and as warp segments, with the bitmask gate and the bf16
+    copy, element-wise at 1e-5 and bitwise reproducible."""
+    rng = np.random.default_rng(300 + f)
+    for g, mode, orc_mode in ((graph(4000, 12.0, 900, 80, 2), gsg.GSG_NORM_ROW_SELF, orc.NORM_ROW_SELF),
+                              (star_plus_random(6000, 1200, 8), gsg.GSG_NORM_SYM_SELF, orc.NORM_SYM_SELF)):
+        A = orc.normalize(g.indptr, g.indices, orc_mode)
+        sg = ctx.upload(g.indptr, g.indices).normalize(mode)
+        X = rng.standard_normal((g.n, f)).astype(np.float32)
+        Hb = rng.standard_normal((g.n, f)).astype(np.float32)
+        Xd = dev(X)
+        assert Xd.stride(0) % 8 == 0 and Xd.data_ptr() % 32 == 0  # the 256-bit gather path
+        Y, Yt = empty(g.n, f), empty(g.n, f)
+        Ylp = torch.zeros((g.n, wl.ld_for(f, 8)), dtype=torch.bfloat16, device="cuda")[:, :f]
+        ctx.spmm(sg, Xd, Y)
+        ctx.spmm(sg, Xd, Yt, transpose=True, mask=dev(Hb), Ylp=Ylp)
+        assert rel_err(host(Y), orc.spmm(A, X)) <= SPMM_TOL
+        ref_t = np.where(Hb > 0, orc.spmm_t(A, X), 0.0)
+        assert rel_err(host(Yt), ref_t) <= SPMM_TOL
+        assert np.array_equal(host(Ylp), torch.from_numpy(host(Yt).astype(np.float32)).bfloat16().float().numpy())
+        Y2 = empty(g.n, f)
+        ctx.spmm(sg, Xd, Y2)
+        assert torch.equal(Y, Y2)
+
+
 def test_spmm_deterministic_and_identity(ctx):
     g = graph(5000, 20.0, 1500, 100, 5)
     sg = ctx.upload(g.indptr, g.indices).normalize()
