@@ -57,7 +57,19 @@ class GCNStep:
         self.prec = {"bf16": GSG_PREC_BF16, "fp32x3": GSG_PREC_FP32X3, "tf32": GSG_PREC_TF32}[precision]
         dev = torch.device("cuda", device)
         bf = self.prec == GSG_PREC_BF16
-        self.W = [padded(dims[l], dims[l + 1], device=dev) for l in range(self.L)]
+        # weights of equal output width (config 4: 200 -> 1024 x 4) are row blocks of one buffer, so
+        # that the per-step bf16 copy of all of them is ONE gsg_to_bf16 call, not one per layer
+        ldw = {ld_for(dims[l + 1]) for l in range(self.L)}
+        self._w_flat = None
+        if len(ldw) == 1 and len({dims[l + 1] for l in range(self.L)}) == 1:
+            ld, rows = ldw.pop(), sum(dims[:self.L])
+            self._w_flat = torch.zeros((rows, ld), dtype=torch.float32, device=dev)[:, :dims[1]]
+            self._wlp_flat = (torch.zeros((rows, ld_for(dims[1], 8)), dtype=torch.bfloat16, device=dev)[:, :dims[1]]
+                              if bf else None)
+            offs = [sum(dims[:l]) for l in range(self.L + 1)]
+            self.W = [self._w_flat[offs[l]:offs[l + 1]] for l in range(self.L)]
+        else:
+            self.W = [padded(dims[l], dims[l + 1], device=dev) for l in range(self.L)]
         if weights is not None:
             for w, src in zip(self.W, weights):
                 w.copy_(torch.as_tensor(src))
@@ -68,7 +80,10 @@ class GCNStep:
         self.Plp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
         # bf16 weight copies, converted once per step and shared by each layer's forward and
         # backward GEMMs (GSG_W_BF16) instead of one conversion per GEMM call
-        self.Wlp = [padded(dims[l], dims[l + 1], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
+        if self._w_flat is not None and bf:
+            self.Wlp = [self._wlp_flat[offs[l]:offs[l + 1]] for l in range(self.L)]
+        else:
+            self.Wlp = [padded(dims[l], dims[l + 1], torch.bfloat16, device=dev) if bf else None for l in range(self.L)]
         # (layer 1's dX has no consumer below it: no bf16 copy)
         self.dXlp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf and l > 0 else None for l in range(self.L)]
         # ReLU bitmasks of H (gsg.h): the forward epilogue writes 1[H > 0] as bits and the
@@ -111,7 +126,9 @@ class GCNStep:
         if normalize:
             sg.normalize(GSG_NORM_ROW_SELF)
         bf = self.prec == GSG_PREC_BF16
-        if bf:
+        if bf and self._w_flat is not None:
+            ctx.to_bf16(self._w_flat, self._wlp_flat)
+        elif bf:
             for w, wl in zip(self.W, self.Wlp):
                 ctx.to_bf16(w, wl)
         Wop = self.Wlp if bf else self.W
