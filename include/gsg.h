@@ -91,10 +91,14 @@ enum {
                               G = Âᵀ dZ, dW = Xᵀ G, dX = (G Wᵀ) ⊙ 1[H_below > 0]. With this
                               flag the P arguments of both calls carry X's role: forward
                               writes Y (n x f_out) into P; backward reads X (n x f_in) from P. */
-  GSG_W_BF16 = 16          /* GSG_PREC_BF16 only: d_W already points to a bf16 copy of W
+  GSG_W_BF16 = 16,         /* GSG_PREC_BF16 only: d_W already points to a bf16 copy of W
                               (row-major f_in x f_out, ldw in bf16 elements, ldw % 8 == 0),
                               e.g. made once per step with gsg_to_bf16 and shared by the
                               layer's forward and backward; no per-call conversion. */
+  GSG_H_BITS = 32          /* backward: d_H points to the layer's own ReLU bitmask (the
+                              forward's d_Hbits, "ReLU bitmask" layout, ldh in 32-bit words,
+                              ldh >= ceil(f_out / 32)) instead of fp32 H; the dZ = dH ⊙ 1[H > 0]
+                              gate then reads 1/32 of the bytes (same result bit for bit). */
 };
 
 /* ---- GEMM epilogues (gsg_gemm) ------------------------------------------------------- */
@@ -273,7 +277,8 @@ GSG_API int gsg_layer_forward(gsg_ctx_t ctx, gsg_subgraph_t sg, int32_t f_in, in
                               float* d_H, int64_t ldh, void* d_Hlp, int64_t ldhlp,
                               uint32_t* d_Hbits, int64_t ldhbits, int precision, int flags);
 /* Backward of one layer given the forward's P and H:
- *   dZ = dH ⊙ 1[H > 0] (skipped with GSG_DH_PREMASKED: dH is dZ),
+ *   dZ = dH ⊙ 1[H > 0] (skipped with GSG_DH_PREMASKED: dH is dZ; GSG_H_BITS: d_H is H's
+ *        ReLU bitmask),
  *   dW = Pᵀ dZ          (f_in x f_out; GSG_ACCUM_DW adds into dW),
  *   dX = Âᵀ (dZ Wᵀ)     (n x f_in; d_dX = NULL skips it, e.g. for layer 1),
  *        ⊙ 1[H_below > 0] when d_Hbelow != NULL, i.e. dX is then the layer below's dZ;

@@ -29,7 +29,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 GSG_OK, GSG_EINVAL, GSG_EGRAPH, GSG_ENOMEM, GSG_ECUDA, GSG_ENCCL, GSG_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
 GSG_NORM_ROW_SELF, GSG_NORM_SYM_SELF, GSG_NORM_ROW, GSG_NORM_VALUES = 0, 1, 2, 3
 GSG_PREC_TF32, GSG_PREC_BF16, GSG_PREC_FP32X3 = 0, 1, 2
-GSG_NO_RELU, GSG_DH_PREMASKED, GSG_ACCUM_DW, GSG_ORDER_A_XW, GSG_W_BF16 = 1, 2, 4, 8, 16
+GSG_NO_RELU, GSG_DH_PREMASKED, GSG_ACCUM_DW, GSG_ORDER_A_XW, GSG_W_BF16, GSG_H_BITS = 1, 2, 4, 8, 16, 32
 GSG_EPI_NONE, GSG_EPI_RELU, GSG_EPI_MASK = 0, 1, 2
 GSG_HEAD_SOFTMAX, GSG_HEAD_SIGMOID = 0, 1
 GSG_K_SPMM, GSG_K_GEMM, GSG_K_NORM, GSG_K_OTHER = 0, 1, 2, 3

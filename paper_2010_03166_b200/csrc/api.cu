@@ -635,7 +635,10 @@ GSG_API int gsg_layer_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int
       lp = c->ws_lp1.ptr;
     }
     float* dzo = need_fp32 ? (float*)c->ws_dZ.ptr : nullptr;
-    if ((rc = mask_launch(c, n, f_out, dH, lddh, H, ldh, dzo, lddz, lp, lddzlp))) return rc;
+    rc = (flags & GSG_H_BITS)
+             ? mask_bits_launch(c, n, f_out, dH, lddh, reinterpret_cast<const uint32_t*>(H), ldh, dzo, lddz, lp, lddzlp)
+             : mask_launch(c, n, f_out, dH, lddh, H, ldh, dzo, lddz, lp, lddzlp);
+    if (rc) return rc;
     dZ = dzo;
     dZlp = lp;
   } else if (bf16 && !dZlp) {
@@ -770,6 +773,7 @@ GSG_API int gsg_sage_backward(gsg_ctx_t c, gsg_subgraph_t sg, int32_t f_in, int3
   GSG_CHECK(f_in >= 1 && fh >= 1 && fh % 4 == 0, GSG_EINVAL, "f_in=%d f_half=%d (f_half %% 4 == 0 required)", f_in, fh);
   GSG_CHECK(X && P && dH && Ws && Wn && dWs && dWn, GSG_EINVAL, "NULL argument");
   GSG_CHECK((flags & GSG_DH_PREMASKED) || H, GSG_EINVAL, "H is needed unless GSG_DH_PREMASKED");
+  GSG_CHECK(!(flags & GSG_H_BITS), GSG_EUNSUPPORTED, "GSG_H_BITS is a gsg_layer_backward flag");
   GSG_CHECK(lddh >= 2 * fh && lddh % 4 == 0, GSG_EINVAL, "lddh must be >= 2 f_half and a multiple of 4");
   DeviceGuard dg(c->device);
   const int n = sg->n;

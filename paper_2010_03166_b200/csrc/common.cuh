@@ -238,6 +238,8 @@ int gather_rows_launch(gsg_ctx* ctx, int rows, int64_t row_bytes, const void* sr
                        const int32_t* idx, void* dst, int64_t dst_pitch);
 int mask_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh, const float* H, int64_t ldh,
                 float* dZ, int64_t lddz, void* dZlp, int64_t lddzlp);
+int mask_bits_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t lddh, const uint32_t* bits,
+                     int64_t ldb, float* dZ, int64_t lddz, void* dZlp, int64_t lddzlp);
 int head_loss_launch(gsg_ctx* ctx, int n, int C, int kind, const float* S, int64_t lds, const void* labels,
                      const float* node_w, float* dS, float* loss);
 void sampler_detach(gsg_ctx* ctx);  // gsg_ctx_destroy: live samples stop returning buffers to it

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import torch
 
-from . import (GSG_DH_PREMASKED, GSG_HEAD_SIGMOID, GSG_HEAD_SOFTMAX, GSG_NORM_ROW_SELF, GSG_ORDER_A_XW,
+from . import (GSG_DH_PREMASKED, GSG_H_BITS, GSG_HEAD_SIGMOID, GSG_HEAD_SOFTMAX, GSG_NORM_ROW_SELF, GSG_ORDER_A_XW,
                GSG_PREC_BF16, GSG_PREC_FP32X3, GSG_PREC_TF32, GSG_W_BF16, Context, Subgraph)
 
 
@@ -88,8 +88,12 @@ class GCNStep:
         self.dXlp = [padded(n_max, dims[l], torch.bfloat16, device=dev) if bf and l > 0 else None for l in range(self.L)]
         # ReLU bitmasks of H (gsg.h): the forward epilogue writes 1[H > 0] as bits and the
         # backward gates (SpMMᵀ of the layer above, the head's dH_L GEMM) read 1/32 of the bytes
+        # (without a head the top layer's bits gate its own dZ = dH ⊙ 1[H > 0] (GSG_H_BITS) where H is
+        # large enough for the saved bytes to matter: config 4 k_mask 33.2 -> 21.6 us; on config 1's
+        # 2000 x 128 layer writing and reading the bits costs ~1 us more than it saves)
         self.Hb = [torch.zeros((n_max, (dims[l + 1] + 31) // 32), dtype=torch.int32, device=dev)
-                   if relu_bits and (l < self.L - 1 or head != "none") else None for l in range(self.L)]
+                   if relu_bits and (l < self.L - 1 or head != "none" or n_max * dims[l + 1] >= (1 << 21)) else None
+                   for l in range(self.L)]
         # all weight gradients in one flat buffer -> one allreduce (a9)
         # (rows padded to 16-byte strides; the padding is reduced along harmlessly)
         shapes = [(dims[l], dims[l + 1]) for l in range(self.L)]
@@ -150,8 +154,8 @@ class GCNStep:
                      self.loss, dHlp=None if self.dHLlp is None else self.dHLlp[:n], precision=self.prec,
                      node_w=node_w, HL_bits=self._hb(self.L - 1, n))
             dH, dHlp, flags = self.dHL[:n], (None if self.dHLlp is None else self.dHLlp[:n]), GSG_DH_PREMASKED
-        else:
-            dH, dHlp, flags = dH_top, None, 0
+        else:  # the caller's dH: the top layer's backward gates it, from H's bitmask when there is one
+            dH, dHlp, flags = dH_top, None, (GSG_H_BITS if self.Hb[-1] is not None else 0)
         for l in range(self.L - 1, -1, -1):
             Hbits = self._hb(l - 1, n) if l > 0 else None
             Hb = self.H[l - 1][:n] if l > 0 and Hbits is None else None
@@ -161,7 +165,8 @@ class GCNStep:
             if o2 and Plp is not None:
                 ctx.to_bf16(inputs[l], Plp)
             dXl = self.dX[l][:n] if (l > 0 or input_grad) else None
-            ctx.layer_backward(sg, Pl, self.H[l][:n], dH, Wop[l], self.dW[l], dXl,
+            Hown = self._hb(l, n) if flags & GSG_H_BITS else self.H[l][:n]
+            ctx.layer_backward(sg, Pl, Hown, dH, Wop[l], self.dW[l], dXl,
                                d[l], d[l + 1], precision=self.prec, Plp=Plp, dHlp=dHlp,
                                dXlp=None if (self.dXlp[l] is None or l == 0) else self.dXlp[l][:n], H_below=Hb,
                                flags=flags | (GSG_ORDER_A_XW if o2 else 0) | wflag, H_below_bits=Hbits)

@@ -424,6 +424,46 @@ def test_layer_w_bf16_flag(ctx, order2):
     assert e.value.code == gsg.GSG_EINVAL
 
 
+@pytest.mark.parametrize("prec,order2", [(gsg.GSG_PREC_TF32, False), (gsg.GSG_PREC_BF16, False),
+                                          (gsg.GSG_PREC_BF16, True), (gsg.GSG_PREC_FP32X3, False)])
+def test_layer_h_bits_flag(ctx, prec, order2):
+    """GSG_H_BITS: the backward's own dZ = dH ⊙ 1[H > 0] gate read from the forward's ReLU bitmask
+    (d_H = H's bits) gives bit-identical dW and dX to the fp32-H gate, at a width with a partial
+    last word (f_out = 100)."""
+    g = graph(4000, 12.0, 900, 80, 23)
+    fi, fo = (96, 100) if not order2 else (128, 100)
+    rng = np.random.default_rng(24)
+    X = rng.standard_normal((g.n, fi)).astype(np.float32)
+    W = (rng.standard_normal((fi, fo)) * 0.1).astype(np.float32)
+    dH = rng.standard_normal((g.n, fo)).astype(np.float32)
+    sg = ctx.upload(g.indptr, g.indices).normalize()
+    Xd, Wd, dHd = dev(X), dev(W), dev(dH)
+    bf = prec == gsg.GSG_PREC_BF16
+    f2 = gsg.GSG_ORDER_A_XW if order2 else 0
+    P = empty(g.n, fo if order2 else fi)
+    H = empty(g.n, fo)
+    Hbits = torch.zeros((g.n, (fo + 31) // 32), dtype=torch.int32, device="cuda")
+    Plp = torch.zeros((g.n, wl.ld_for(fi, 8)), dtype=torch.bfloat16, device="cuda")[:, :fi] if bf else None
+    ctx.layer_forward(sg, Xd, Wd, P, H, fi, fo, precision=prec, Plp=None if order2 else Plp, flags=f2,
+                      H_bits=Hbits)
+    if order2 and bf:
+        ctx.to_bf16(Xd, Plp)
+    outs = []
+    for Hop, fl in ((H, 0), (Hbits, gsg.GSG_H_BITS)):
+        dW, dX = empty(fi, fo), empty(g.n, fi)
+        ctx.layer_backward(sg, Xd if order2 else P, Hop, dHd, Wd, dW, dX, fi, fo, precision=prec, Plp=Plp,
+                           flags=f2 | fl)
+        outs.append([host(t) for t in (dW, dX)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    Hh = host(H)
+    dZ = np.where(Hh > 0, dH, 0.0)
+    ref_dW = orc.gemm(orc.spmm(orc.normalize(g.indptr, g.indices, orc.NORM_ROW_SELF), X), dZ, transA=True) \
+        if not order2 else None
+    if ref_dW is not None:
+        assert rel_err(outs[1][0], ref_dW) <= GEMM_TOL
+
+
 def test_layer_end_to_end_config1(ctx):
     cfg = wl.CONFIGS[1]
     g = wl.sample_subgraph(cfg)
