@@ -35,28 +35,27 @@ __global__ void k_mask(int rows, int cols4, const float4* __restrict__ dH, int64
 }
 
 // dZ = dH ⊙ 1[H > 0] with the gate read from H's ReLU bitmask (GSG_H_BITS): one thread per (row,
-// float4 column); 8 consecutive threads share one 32-bit word. Row-major 2D grid-stride (no 64-bit
-// division per element).
-__global__ void k_mask_bits(int rows, int cols4, const float4* __restrict__ dH, int64_t lddh4,
+// float4 column) over the flattened rows x cols4 range (32-bit index: the host checks the size);
+// 8 consecutive threads share one 32-bit word.
+__global__ void k_mask_bits(uint32_t total, uint32_t cols4, const float4* __restrict__ dH, int64_t lddh4,
                             const uint32_t* __restrict__ bits, int64_t ldb, float4* __restrict__ dZ, int64_t lddz4,
                             uint2* __restrict__ dZlp, int64_t lddzlp4) {
-  for (int r = blockIdx.y; r < rows; r += gridDim.y) {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols4; c += gridDim.x * blockDim.x) {
-      const float4 g = __ldg(dH + (int64_t)r * lddh4 + c);
-      const uint32_t m = __ldg(bits + (int64_t)r * ldb + (c >> 3)) >> ((c & 7) * 4);
-      float4 z;
-      z.x = m & 1u ? g.x : 0.f;
-      z.y = m & 2u ? g.y : 0.f;
-      z.z = m & 4u ? g.z : 0.f;
-      z.w = m & 8u ? g.w : 0.f;
-      if (dZ) dZ[(int64_t)r * lddz4 + c] = z;
-      if (dZlp) {
-        __nv_bfloat162 lo = __floats2bfloat162_rn(z.x, z.y), hi = __floats2bfloat162_rn(z.z, z.w);
-        uint2 p;
-        p.x = *reinterpret_cast<uint32_t*>(&lo);
-        p.y = *reinterpret_cast<uint32_t*>(&hi);
-        dZlp[(int64_t)r * lddzlp4 + c] = p;
-      }
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t r = i / cols4, c = i - r * cols4;
+    const float4 g = __ldg(dH + (int64_t)r * lddh4 + c);
+    const uint32_t m = __ldg(bits + (int64_t)r * ldb + (c >> 3)) >> ((c & 7) * 4);
+    float4 z;
+    z.x = m & 1u ? g.x : 0.f;
+    z.y = m & 2u ? g.y : 0.f;
+    z.z = m & 4u ? g.z : 0.f;
+    z.w = m & 8u ? g.w : 0.f;
+    if (dZ) dZ[(int64_t)r * lddz4 + c] = z;
+    if (dZlp) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(z.x, z.y), hi = __floats2bfloat162_rn(z.z, z.w);
+      uint2 p;
+      p.x = *reinterpret_cast<uint32_t*>(&lo);
+      p.y = *reinterpret_cast<uint32_t*>(&hi);
+      dZlp[(int64_t)r * lddzlp4 + c] = p;
     }
   }
 }
@@ -291,14 +290,12 @@ int mask_bits_launch(gsg_ctx* ctx, int rows, int cols, const float* dH, int64_t 
             "mask: strides must be multiples of 4 (bf16: 8), bitmask ldh >= ceil(f/32) words");
   if (rows == 0 || cols == 0) return GSG_OK;
   ProfScope ps(ctx, GSG_K_OTHER, (4.0 + 0.125 + (dZ ? 4.0 : 0.0) + (dZlp ? 2.0 : 0.0)) * rows * cols, 0.0);
-  const int cols4 = (cols + 3) / 4;
-  const int bx = (cols4 + 255) / 256;
-  int by = rows;
-  const int cap = ctx->num_sms * 8;
-  if ((int64_t)bx * by > cap) by = std::max(1, cap / bx);
-  if (by > 65535) by = 65535;
-  k_mask_bits<<<dim3(bx, by), 256, 0, ctx->stream>>>(rows, cols4, (const float4*)dH, lddh / 4, bits, ldb,
-                                                     (float4*)dZ, lddz / 4, (uint2*)dZlp, lddzlp / 4);
+  const int64_t cols4 = (cols + 3) / 4, total = (int64_t)rows * cols4;
+  GSG_CHECK(total < ((int64_t)1 << 31), GSG_EUNSUPPORTED, "mask: rows x ceil(f/4) >= 2^31");
+  int grid = (int)((total + 255) / 256);
+  if (grid > ctx->num_sms * 8) grid = ctx->num_sms * 8;
+  k_mask_bits<<<grid, 256, 0, ctx->stream>>>((uint32_t)total, (uint32_t)cols4, (const float4*)dH, lddh / 4, bits, ldb,
+                                             (float4*)dZ, lddz / 4, (uint2*)dZlp, lddzlp / 4);
   count_launch(ctx);
   GSG_CUDA(cudaGetLastError());
   return GSG_OK;

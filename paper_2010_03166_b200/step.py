@@ -14,6 +14,8 @@ subgraph; the step itself allocates nothing (CUDA-graph friendly).
 """
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import (GSG_DH_PREMASKED, GSG_H_BITS, GSG_HEAD_SIGMOID, GSG_HEAD_SOFTMAX, GSG_NORM_ROW_SELF, GSG_ORDER_A_XW,
@@ -89,10 +91,13 @@ class GCNStep:
         # ReLU bitmasks of H (gsg.h): the forward epilogue writes 1[H > 0] as bits and the
         # backward gates (SpMMᵀ of the layer above, the head's dH_L GEMM) read 1/32 of the bytes
         # (without a head the top layer's bits gate its own dZ = dH ⊙ 1[H > 0] (GSG_H_BITS) where H is
-        # large enough for the saved bytes to matter: config 4 k_mask 33.2 -> 21.6 us; on config 1's
-        # 2000 x 128 layer writing and reading the bits costs ~1 us more than it saves)
+        # large enough for the saved bytes to matter: config 4 k_mask 33.2 -> 21.6 us, step 1.906 ->
+        # 1.891 ms, batched config 1 (x64) 0.447 -> 0.434 ms; on config 1's single 2000 x 128 layer
+        # writing and reading the bits costs ~1 us more than it saves)
+        top_bits = os.environ.get("GSG_STEP_TOP_BITS", "1") != "0"  # A/B
         self.Hb = [torch.zeros((n_max, (dims[l + 1] + 31) // 32), dtype=torch.int32, device=dev)
-                   if relu_bits and (l < self.L - 1 or head != "none" or n_max * dims[l + 1] >= (1 << 21)) else None
+                   if relu_bits and (l < self.L - 1 or head != "none" or (top_bits and n_max * dims[l + 1] >= (1 << 21)))
+                   else None
                    for l in range(self.L)]
         # all weight gradients in one flat buffer -> one allreduce (a9)
         # (rows padded to 16-byte strides; the padding is reduced along harmlessly)
