@@ -868,10 +868,19 @@ int spmm_launch(gsg_ctx* ctx, const gsg_subgraph* sg, int transpose, int f, cons
     }
     const int64_t tasks = (int64_t)sg->n * a.nchunks;
     static const int minb_env = getenv("GSG_SPMM_MINB") ? atoi(getenv("GSG_SPMM_MINB")) : 0;  // A/B: force 2 or 3
-    // three CTAs per SM from ~4 (row, chunk) tasks per warp on: config 5 / 4 f = 200 (20000 / 16000
-    // tasks) 125.5 -> 119.9 / 52.6 -> 50.8 us; config 3 f = 200 (12000 tasks) stays at two
-    // (35.8 vs 38.4 us); profiles/r02_spmm_variants_ab.txt
-    const bool three = minb_env == 3 || (minb_env != 2 && tasks >= 4LL * ctx->num_sms * 3 * kWarps);
+    // (static schedule: three CTAs per SM from ~4 (row, chunk) tasks per warp on -- config 5 / 4
+    // f = 200 125.5 -> 119.9 / 52.6 -> 50.8 us; profiles/r02_spmm_variants_ab.txt)
+    // With dynamically claimed tasks (a.dyn) two CTAs/SM (128 registers) gather as fast or faster
+    // on launches of one or two column chunks (f <= 512: config 5 f = 200 111.0 -> 109.5 us alone,
+    // config 3 f = 512 56.8 -> 53.0; steps: config 2 0.480 -> 0.463 ms, config 3 0.552 -> 0.531,
+    // config 5 2.787 -> 2.785), except for the lane-group remainder launches (f = 300 168.8 ->
+    // 176.0 at two); the 4-chunk f = 1024 launches keep three (in-step neutral to slightly worse
+    // at two). profiles/r02_spmm_occupancy_dyn_ab.txt. GSG_SPMM_OCC_RULE (A/B): 0 the
+    // static-schedule rule (three from ~4 tasks per warp on), 1 two for every non-remainder launch.
+    static const int occ_rule = getenv("GSG_SPMM_OCC_RULE") ? atoi(getenv("GSG_SPMM_OCC_RULE")) : 2;
+    const bool many = tasks >= 4LL * ctx->num_sms * 3 * kWarps;
+    const bool two_ok = a.dyn && !a.tailg && (occ_rule == 1 || (occ_rule == 2 && a.nchunks <= 2));
+    const bool three = minb_env == 3 || (minb_env != 2 && many && !two_ok);
     static const int u_env = getenv("GSG_SPMM_U") ? atoi(getenv("GSG_SPMM_U")) : 8;  // A/B: gathers in flight
     static std::atomic<int> occ36{0}, occ44{0};
     if (a.w256 && minb_env == 4) return launch_k(ctx, k_spmm_wide<4, true, 4>, &occ44, a, tasks);
