@@ -191,7 +191,10 @@ __global__ void k_bin_scatter(int n, const int32_t* __restrict__ rowptr, int32_t
 int hseg_len(const gsg_ctx* ctx, int64_t nnz_hat) {
   static const int env = getenv("GSG_HSEG_LEN") ? atoi(getenv("GSG_HSEG_LEN")) : 0;
   if (env >= 32) return env;
-  const int64_t per_warp = nnz_hat / ((int64_t)ctx->num_sms * 24);
+  // 16 warps per SM: the f <= 512 launches run two 8-warp CTAs/SM since the dynamic schedule, and
+  // with claimed tasks longer segments cost less than the combines they save (config 4 192 -> 256:
+  // 1.903 -> 1.874 ms; config 3 stays within 0.3 % at 192; profiles/r02_hseg_len_ab.txt)
+  const int64_t per_warp = nnz_hat / ((int64_t)ctx->num_sms * 16);
   const int64_t v = (per_warp + 31) / 32 * 32;  // rounded up to whole 32-neighbor groups
   return (int)std::min<int64_t>(kHSeg, std::max<int64_t>(160, v));
 }
